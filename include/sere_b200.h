@@ -1,0 +1,170 @@
+/*
+ * sere_b200.h -- C-ABI of the B200-native SERE batched-decode MoE path.
+ *
+ * The reference (`/root/reference/pkg/src/sere`) is pure Python; it has no FFI.
+ * Its operator boundary is two module-level functions that `moe.model_forward`
+ * resolves at call time (moe.py:368 and moe.py:375):
+ *
+ *   rerouting.apply_sere(assignment, sim, config) -> RerouteResult   (rerouting.py:130-171)
+ *   moe.layer_forward(layer, x, assignment, activation) -> ndarray    (moe.py:280-310)
+ *
+ * Every entry point below replaces one of those (or a stage inside them) and is
+ * what a ctypes binding of the reference would call.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers, caller-owned, dense row-major.
+ *    The library never frees caller memory and keeps no pointer after the
+ *    stream work completes. `stream` is a cudaStream_t (NULL = legacy stream).
+ *  - Every call is asynchronous and stream-ordered; none synchronises the host.
+ *  - Return value: host-side status (shape/config checks, launch errors).
+ *    Data-dependent checks that the reference performs on every call (ids out
+ *    of range, similarity outside [0,1]) run on the device and are reported
+ *    through `status_dev` (one int32, device memory, SERE_OK on success); read
+ *    it after the stream completes. Kernels downstream of a failed check do no
+ *    work. Codes map 1:1 onto the reference exceptions (errors.py:9-34).
+ *  - Expert ids are int32 (the reference uses int64; values are identical).
+ *  - bf16 tensors are passed as uint16_t* (raw bf16 bits).
+ */
+#ifndef SERE_B200_H_
+#define SERE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SERE_ABI_VERSION 1
+
+/* status codes  (paper_2602_07616_b200/errors.py keeps the same numbers) */
+enum {
+  SERE_OK = 0,
+  SERE_ERR_CONFIG = 1,      /* ConfigError    : S<1, S>K, rho outside [0,1], bad activation */
+  SERE_ERR_DIMENSION = 2,   /* DimensionError : shapes; id outside [0,M) in re-routing (rerouting.py:111-114) */
+  SERE_ERR_INPUT = 3,       /* InputError     : similarity outside [0,1] (rerouting.py:115-116) */
+  SERE_ERR_ROUTING = 4,     /* RoutingError   : id outside [0,M) in layer_forward (moe.py:299-300) */
+  SERE_ERR_DOMAIN = 5,      /* DomainError    : non-finite inputs */
+  SERE_ERR_CUDA = 6,        /* CUDA launch / runtime failure */
+  SERE_ERR_UNSUPPORTED = 7, /* device is not sm_100 / limits exceeded */
+  SERE_ERR_WORKSPACE = 8    /* workspace too small */
+};
+
+/* per-expert classification written by sere_reroute (bit flags) */
+enum {
+  SERE_CLASS_PRIMARY = 1,  /* in the batch primary set (union of slots < S)      rerouting.py:147 */
+  SERE_CLASS_CRITICAL = 2, /* secondary kept because best sim < rho (rho > 0)    rerouting.py:160-161 */
+  SERE_CLASS_REROUTED = 4  /* secondary redirected; target in reroute_map[e]    rerouting.py:162-164 */
+};
+
+/* activations of moe.py:22 */
+enum { SERE_ACT_SILU = 0, SERE_ACT_RELU = 1, SERE_ACT_GELU_TANH = 2 };
+
+/* flags for sere_reroute / sere_moe_forward */
+enum {
+  SERE_FLAG_CHECK_SIM = 1 /* validate sim in [0,1] on the device (InputError); the Python
+                             mirror validates once per uploaded matrix instead */
+};
+
+int sere_abi_version(void);
+const char* sere_status_string(int status);
+
+/* Returns SERE_OK iff `device` is an sm_100 part the kernels were built for. */
+int sere_device_check(int device);
+
+/* ------------------------------------------------------------------------
+ * (1) Re-routing.  Replaces rerouting.apply_sere (rerouting.py:130-171),
+ *     equivalently the Alg. 2 kernel contract apply_sere_parallel (174-249).
+ *
+ *  ids_in     int32 [T,K]  top-k expert ids, slot 0 strongest (RoutingAssignment.indices)
+ *  sim        f64   [M,M]  similarity, row = secondary u, column = candidate v
+ *  S, rho     retain_count and threshold of RerouteConfig (rerouting.py:31-54)
+ *  ids_out    int32 [T,K]  RerouteResult.new_indices, bit-exact
+ *  expert_class u8 [M]     SERE_CLASS_* flags (0 = expert not routed to)
+ *  reroute_map int32 [M]   target of a SERE_CLASS_REROUTED expert, else -1
+ *                          (reference NaN quirk: a rerouted expert may map to -1)
+ *  active_list int32 [M]   final_active, ascending; n_active int32[1] its length
+ *  Weights are never read nor written (the reference leaves them untouched).
+ * ------------------------------------------------------------------------ */
+int sere_reroute(const int32_t* ids_in, const double* sim, int T, int K, int M, int S, double rho,
+                 int flags, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map,
+                 int32_t* active_list, int32_t* n_active, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (2) Expert bank: the layer's routed experts [0,M) followed by its shared
+ *     experts [M, M+n_shared), bf16, in the tcgen05 tile layout.
+ *     sere_pack_experts converts `count` experts from the reference orientation
+ *     (ExpertWeights moe.py:70-77: w_gate,w_up [d_h,d_m], w_down [d_m,d_h],
+ *     row-major, here bf16) into bank slots [first, first+count).
+ * ------------------------------------------------------------------------ */
+size_t sere_expert_bank_bytes(int n_experts_total, int d_h, int d_m);
+int sere_pack_experts(const uint16_t* w_gate, const uint16_t* w_up, const uint16_t* w_down, int count,
+                      int d_h, int d_m, void* bank, int n_experts_total, int first, void* stream);
+/* Inverse of sere_pack_experts (for checkpoints / tests). */
+int sere_unpack_experts(const void* bank, int n_experts_total, int first, int count, int d_h, int d_m,
+                        uint16_t* w_gate, uint16_t* w_up, uint16_t* w_down, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (3) MoE layer forward.  Replaces moe.layer_forward (moe.py:280-310):
+ *     y[t] = sum_k w[t,k] * E_{ids[t,k]}(x[t])  (slot order 0..K-1)  + sum_s E_shared_s(x[t])
+ *     E(x) = act(x Wg) * (x Wu) Wd.  Duplicate ids in a row contribute once per slot.
+ *
+ *  x          bf16 [T,d_h];  ids int32 [T,K];  weights f32 [T,K]
+ *  y          f32  [T,d_h]   (required);  y_bf16 bf16 [T,d_h] (optional, may be NULL)
+ *  workspace  >= sere_layer_workspace_bytes(...) bytes, 256-B aligned.
+ *  Data-dependent error: id outside [0,M) -> SERE_ERR_ROUTING in status_dev.
+ * ------------------------------------------------------------------------ */
+size_t sere_layer_workspace_bytes(int T, int K, int M, int n_shared, int d_h, int d_m);
+int sere_layer_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation,
+                       const uint16_t* x, const int32_t* ids, const float* weights, int T, int K,
+                       float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
+                       int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (4) Fused SERE layer: sere_reroute + sere_layer_forward on the rewritten ids
+ *     (the body of moe.model_forward's loop, moe.py:367-375) with the
+ *     re-routing, count/align and permute fused into one launch pair.
+ *     Pass S == K (or rho == 1 with off-diagonal sims < 1) for plain top-k on
+ *     the same kernels.  Re-routing outputs as in sere_reroute (all optional
+ *     except ids_out may be NULL too).
+ * ------------------------------------------------------------------------ */
+int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation,
+                     const double* sim, int S, double rho, int flags, const uint16_t* x,
+                     const int32_t* ids_in, const float* weights, int T, int K, int32_t* ids_out,
+                     uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
+                     int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace,
+                     size_t workspace_bytes, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (5) Router: logits = x W_r (fp32 accumulate), top-K with ties to the lower
+ *     index, softmax over the K picks.  Replaces moe.route_topk / topk_softmax
+ *     (moe.py:248-277).  w_router bf16 [d_h, M] (reference orientation).
+ * ------------------------------------------------------------------------ */
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router, int T, int d_h, int M, int K,
+                    int32_t* ids, float* weights, float* logits_out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Introspection of the workspace (tests read the count/align plan back).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  size_t off_plan_i32;   /* int32 plan header + arrays              */
+  size_t off_slot_row;   /* int32 [T*(K+n_shared)] permuted row of every (token, slot) */
+  size_t off_row_token;  /* int32 [R_max] source token of each permuted row, -1 = pad */
+  size_t off_x_pack;     /* bf16 [d_h_pad/64][R_max][64] swizzled activations          */
+  size_t off_h_pack;     /* bf16 [d_m_pad/64][R_max][64] swizzled SwiGLU output        */
+  size_t off_y_perm;     /* f32  [ksplit][R_max][d_h_pad] expert outputs               */
+  size_t total_bytes;
+  int32_t r_max;         /* rows reserved for the permuted batch                        */
+  int32_t d_h_pad, d_m_pad, ksplit_down;
+  int32_t plan_groups_off; /* int32 offsets (in elements) inside the plan block: */
+  int32_t plan_group_expert_off, plan_group_row0_off, plan_group_rows_off;
+  int32_t plan_counts_off, plan_unit_off_gu, plan_unit_off_dn;
+} sere_ws_layout;
+
+int sere_layer_workspace_layout(int T, int K, int M, int n_shared, int d_h, int d_m,
+                                sere_ws_layout* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SERE_B200_H_ */

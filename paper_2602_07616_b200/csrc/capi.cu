@@ -1,0 +1,317 @@
+// capi.cu -- extern "C" entry points of include/sere_b200.h: host-side checks
+// (shape/config, in the reference's order), workspace carving, launch sequencing.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "../../include/sere_b200.h"
+#include "params.cuh"
+#include "plan.cuh"
+
+namespace sere {
+
+namespace {
+
+constexpr int kMaxCells = 16384;  // T*K limit of the single-CTA align kernel (u16 counters, 64 KB ids)
+constexpr int kMaxExperts = 1024;
+constexpr int kMaxShared = 31;
+
+int g_num_sms[64] = {0};
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (g_num_sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_num_sms[dev] = n > 0 ? n : 148;
+  }
+  return g_num_sms[dev];
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t plan, slot_row, row_token, x_pack, h_pack, y_perm, total;
+  int r_max;
+  Dims d;
+  int Et;
+};
+
+WsLayout ws_layout(int T, int K, int M, int n_shared, int d_h, int d_m) {
+  WsLayout L;
+  L.d = make_dims(d_h, d_m);
+  L.Et = M + n_shared;
+  L.r_max = round_up(T * (K + n_shared) + kRowAlign * L.Et, 8);
+  const PlanOffsets po = plan_offsets(L.Et);
+  size_t off = 0;
+  L.plan = off;
+  off = align_up(off + static_cast<size_t>(po.total) * 4, 1024);
+  L.slot_row = off;
+  off = align_up(off + static_cast<size_t>(T) * (K + n_shared) * 4, 1024);
+  L.row_token = off;
+  off = align_up(off + static_cast<size_t>(L.r_max) * 4, 1024);
+  L.x_pack = off;
+  off = align_up(off + static_cast<size_t>(L.d.ktiles_gu) * L.r_max * 128, 1024);
+  L.h_pack = off;
+  off = align_up(off + static_cast<size_t>(L.d.ktiles_dn) * L.r_max * 128, 1024);
+  L.y_perm = off;
+  off = align_up(off + static_cast<size_t>(L.d.ksplit_dn) * L.r_max * L.d.d_h_pad * 4, 1024);
+  L.total = off + 1024;  // slack for aligning the caller's base to 1024 B
+  return L;
+}
+
+int check_cuda(cudaError_t e) { return e == cudaSuccess ? SERE_OK : SERE_ERR_CUDA; }
+
+int check_layer_shapes(int M, int n_shared, int d_h, int d_m, int activation, int T, int K) {
+  if (M < 1 || M > kMaxExperts || n_shared < 0 || n_shared > kMaxShared) return SERE_ERR_UNSUPPORTED;
+  if (d_h < 1 || d_m < 1) return SERE_ERR_CONFIG;
+  if (activation < SERE_ACT_SILU || activation > SERE_ACT_GELU_TANH) return SERE_ERR_CONFIG;
+  if (T < 0 || K < 1) return SERE_ERR_DIMENSION;
+  if (K > M) return SERE_ERR_CONFIG;  // top_k <= M (moe.py:116-118)
+  if (static_cast<long long>(T) * K > kMaxCells) return SERE_ERR_UNSUPPORTED;
+  return SERE_OK;
+}
+
+int check_reroute_cfg(int K, int M, int S, double rho) {
+  if (S < 1) return SERE_ERR_CONFIG;                         // rerouting.py:45-46
+  if (!(rho >= 0.0 && rho <= 1.0)) return SERE_ERR_CONFIG;   // rerouting.py:48-49 (NaN rejected too)
+  if (S > K) return SERE_ERR_CONFIG;                         // rerouting.py:104-107
+  if (M < 1 || M > kMaxExperts) return SERE_ERR_UNSUPPORTED;
+  return SERE_OK;
+}
+
+int run_layer(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, const double* sim, int S,
+              double rho, int flags, int mode, const uint16_t* x, const int32_t* ids_in, const float* weights,
+              int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
+              int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
+              int32_t* status_dev, cudaStream_t stream) {
+  const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
+  if (workspace == nullptr || workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
+  if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr || y == nullptr)
+    return SERE_ERR_DIMENSION;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(align_up(reinterpret_cast<uintptr_t>(workspace), 1024));
+  int32_t* plan = reinterpret_cast<int32_t*>(ws + L.plan);
+  int32_t* slot_row = reinterpret_cast<int32_t*>(ws + L.slot_row);
+  int32_t* row_token = reinterpret_cast<int32_t*>(ws + L.row_token);
+  uint8_t* x_pack = ws + L.x_pack;
+  uint8_t* h_pack = ws + L.h_pack;
+  float* y_perm = reinterpret_cast<float*>(ws + L.y_perm);
+  const Dims& d = L.d;
+  const int sms = num_sms();
+
+  AlignParams ap{};
+  ap.ids_in = ids_in;
+  ap.sim = sim;
+  ap.T = T; ap.K = K; ap.M = M; ap.S = S; ap.n_shared = n_shared;
+  ap.rho = rho;
+  ap.flags = flags;
+  ap.mode = mode;
+  ap.ids_out = ids_out;
+  ap.expert_class = expert_class;
+  ap.reroute_map = reroute_map;
+  ap.active_list = active_list;
+  ap.n_active = n_active;
+  ap.status_dev = status_dev;
+  ap.plan = plan;
+  ap.slot_row = slot_row;
+  ap.row_token = row_token;
+  ap.tiles_gu = d.tiles_gu;
+  ap.units_dn_per = d.tiles_dn * d.ksplit_dn;
+  cudaError_t e = launch_reroute_align(ap, stream);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
+
+  e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
+
+  const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
+  const uint8_t* w2 = w13 + bank_w13_bytes(L.Et, d);
+  GemmParams gp{};
+  gp.a_base = w13;
+  gp.tiles_m = d.tiles_gu;
+  gp.ktiles = d.ktiles_gu;
+  gp.ksplit = 1;
+  gp.b_base = x_pack;
+  gp.r_max = L.r_max;
+  gp.plan = plan;
+  gp.Et = L.Et;
+  gp.which = 0;
+  gp.epi = 0;
+  gp.act = activation;
+  gp.h_pack = h_pack;
+  gp.y_perm = y_perm;
+  gp.d_h_pad = d.d_h_pad;
+  e = launch_grouped_gemm(gp, sms, stream);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
+
+  gp.a_base = w2;
+  gp.tiles_m = d.tiles_dn;
+  gp.ktiles = d.ktiles_dn;
+  gp.ksplit = d.ksplit_dn;
+  gp.b_base = h_pack;
+  gp.which = 1;
+  gp.epi = 1;
+  e = launch_grouped_gemm(gp, sms, stream);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
+
+  e = launch_combine(y_perm, d, L.r_max, plan, slot_row, weights, T, K, n_shared, y,
+                     reinterpret_cast<__nv_bfloat16*>(y_bf16), stream);
+  return check_cuda(e);
+}
+
+}  // namespace
+}  // namespace sere
+
+using namespace sere;
+
+extern "C" {
+
+int sere_abi_version(void) { return SERE_ABI_VERSION; }
+
+const char* sere_status_string(int status) {
+  switch (status) {
+    case SERE_OK: return "ok";
+    case SERE_ERR_CONFIG: return "ConfigError";
+    case SERE_ERR_DIMENSION: return "DimensionError";
+    case SERE_ERR_INPUT: return "InputError";
+    case SERE_ERR_ROUTING: return "RoutingError";
+    case SERE_ERR_DOMAIN: return "DomainError";
+    case SERE_ERR_CUDA: return "CUDA error";
+    case SERE_ERR_UNSUPPORTED: return "unsupported device or size";
+    case SERE_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int sere_device_check(int device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SERE_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return SERE_ERR_UNSUPPORTED;
+  return SERE_OK;
+}
+
+int sere_reroute(const int32_t* ids_in, const double* sim, int T, int K, int M, int S, double rho, int flags,
+                 int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
+                 int32_t* n_active, int32_t* status_dev, void* stream) {
+  if (T < 0 || K < 1) return SERE_ERR_DIMENSION;
+  const int rc = check_reroute_cfg(K, M, S, rho);
+  if (rc != SERE_OK) return rc;
+  if (static_cast<long long>(T) * K > kMaxCells) return SERE_ERR_UNSUPPORTED;
+  if ((ids_in == nullptr && T > 0) || sim == nullptr) return SERE_ERR_DIMENSION;
+  AlignParams ap{};
+  ap.ids_in = ids_in;
+  ap.sim = sim;
+  ap.T = T; ap.K = K; ap.M = M; ap.S = S; ap.n_shared = 0;
+  ap.rho = rho;
+  ap.flags = flags;
+  ap.mode = MODE_REROUTE;
+  ap.ids_out = ids_out;
+  ap.expert_class = expert_class;
+  ap.reroute_map = reroute_map;
+  ap.active_list = active_list;
+  ap.n_active = n_active;
+  ap.status_dev = status_dev;
+  return check_cuda(launch_reroute_align(ap, static_cast<cudaStream_t>(stream)));
+}
+
+size_t sere_expert_bank_bytes(int n_experts_total, int d_h, int d_m) {
+  if (n_experts_total < 1 || d_h < 1 || d_m < 1) return 0;
+  const Dims d = make_dims(d_h, d_m);
+  return bank_w13_bytes(n_experts_total, d) + bank_w2_bytes(n_experts_total, d);
+}
+
+int sere_pack_experts(const uint16_t* w_gate, const uint16_t* w_up, const uint16_t* w_down, int count, int d_h,
+                      int d_m, void* bank, int n_experts_total, int first, void* stream) {
+  if (count < 0 || first < 0 || first + count > n_experts_total || d_h < 1 || d_m < 1) return SERE_ERR_DIMENSION;
+  if (bank == nullptr || (count > 0 && (!w_gate || !w_up || !w_down))) return SERE_ERR_DIMENSION;
+  const Dims d = make_dims(d_h, d_m);
+  return check_cuda(launch_pack(reinterpret_cast<const __nv_bfloat16*>(w_gate),
+                                reinterpret_cast<const __nv_bfloat16*>(w_up),
+                                reinterpret_cast<const __nv_bfloat16*>(w_down), count, d, n_experts_total, first,
+                                reinterpret_cast<uint8_t*>(bank), 0, static_cast<cudaStream_t>(stream)));
+}
+
+int sere_unpack_experts(const void* bank, int n_experts_total, int first, int count, int d_h, int d_m,
+                        uint16_t* w_gate, uint16_t* w_up, uint16_t* w_down, void* stream) {
+  if (count < 0 || first < 0 || first + count > n_experts_total || d_h < 1 || d_m < 1) return SERE_ERR_DIMENSION;
+  if (bank == nullptr || (count > 0 && (!w_gate || !w_up || !w_down))) return SERE_ERR_DIMENSION;
+  const Dims d = make_dims(d_h, d_m);
+  return check_cuda(launch_pack(reinterpret_cast<const __nv_bfloat16*>(w_gate),
+                                reinterpret_cast<const __nv_bfloat16*>(w_up),
+                                reinterpret_cast<const __nv_bfloat16*>(w_down), count, d, n_experts_total, first,
+                                reinterpret_cast<uint8_t*>(const_cast<void*>(bank)), 1,
+                                static_cast<cudaStream_t>(stream)));
+}
+
+size_t sere_layer_workspace_bytes(int T, int K, int M, int n_shared, int d_h, int d_m) {
+  if (T < 0 || K < 1 || M < 1 || n_shared < 0 || d_h < 1 || d_m < 1) return 0;
+  return ws_layout(T, K, M, n_shared, d_h, d_m).total;
+}
+
+int sere_layer_workspace_layout(int T, int K, int M, int n_shared, int d_h, int d_m, sere_ws_layout* out) {
+  if (out == nullptr || T < 0 || K < 1 || M < 1 || n_shared < 0 || d_h < 1 || d_m < 1) return SERE_ERR_DIMENSION;
+  const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
+  const PlanOffsets po = plan_offsets(L.Et);
+  out->off_plan_i32 = L.plan;
+  out->off_slot_row = L.slot_row;
+  out->off_row_token = L.row_token;
+  out->off_x_pack = L.x_pack;
+  out->off_h_pack = L.h_pack;
+  out->off_y_perm = L.y_perm;
+  out->total_bytes = L.total;
+  out->r_max = L.r_max;
+  out->d_h_pad = L.d.d_h_pad;
+  out->d_m_pad = L.d.d_m_pad;
+  out->ksplit_down = L.d.ksplit_dn;
+  out->plan_groups_off = P_NGROUPS;
+  out->plan_group_expert_off = po.group_expert;
+  out->plan_group_row0_off = po.group_row0;
+  out->plan_group_rows_off = po.group_rows;
+  out->plan_counts_off = po.counts;
+  out->plan_unit_off_gu = po.unit_off_gu;
+  out->plan_unit_off_dn = po.unit_off_dn;
+  return SERE_OK;
+}
+
+int sere_layer_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, const uint16_t* x,
+                       const int32_t* ids, const float* weights, int T, int K, float* y, uint16_t* y_bf16,
+                       void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream) {
+  const int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
+  if (rc != SERE_OK) return rc;
+  if (T == 0) return SERE_OK;
+  return run_layer(bank, M, n_shared, d_h, d_m, activation, nullptr, K, 0.0, 0, MODE_ALIGN, x, ids, weights, T, K,
+                   nullptr, nullptr, nullptr, nullptr, nullptr, y, y_bf16, workspace, workspace_bytes, status_dev,
+                   static_cast<cudaStream_t>(stream));
+}
+
+int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, const double* sim,
+                     int S, double rho, int flags, const uint16_t* x, const int32_t* ids_in, const float* weights,
+                     int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map,
+                     int32_t* active_list, int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace,
+                     size_t workspace_bytes, int32_t* status_dev, void* stream) {
+  int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
+  if (rc != SERE_OK) return rc;
+  rc = check_reroute_cfg(K, M, S, rho);
+  if (rc != SERE_OK) return rc;
+  if (sim == nullptr) return SERE_ERR_DIMENSION;
+  if (T == 0) return SERE_OK;
+  return run_layer(bank, M, n_shared, d_h, d_m, activation, sim, S, rho, flags, MODE_REROUTE | MODE_ALIGN, x,
+                   ids_in, weights, T, K, ids_out, expert_class, reroute_map, active_list, n_active, y, y_bf16,
+                   workspace, workspace_bytes, status_dev, static_cast<cudaStream_t>(stream));
+}
+
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router, int T, int d_h, int M, int K, int32_t* ids,
+                    float* weights, float* logits_out, void* stream) {
+  if (T < 0 || d_h < 1 || M < 1 || K < 1) return SERE_ERR_DIMENSION;
+  if (K > M || K > 32 || M > kMaxExperts) return K > M ? SERE_ERR_CONFIG : SERE_ERR_UNSUPPORTED;
+  if (T == 0) return SERE_OK;
+  if (!x || !w_router || !ids || !weights) return SERE_ERR_DIMENSION;
+  return check_cuda(launch_route_topk(reinterpret_cast<const __nv_bfloat16*>(x),
+                                      reinterpret_cast<const __nv_bfloat16*>(w_router), T, d_h, M, K, ids, weights,
+                                      logits_out, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// params.cuh -- launch parameter blocks shared by the kernels and capi.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "plan.cuh"
+
+namespace sere {
+
+enum : int { MODE_REROUTE = 1, MODE_ALIGN = 2 };
+enum : int { EPI_SWIGLU = 0, EPI_STORE_F32 = 1 };
+
+struct AlignParams {
+  const int32_t* ids_in;
+  const double* sim;
+  int T, K, M, S, n_shared;
+  double rho;
+  int flags, mode;
+  // re-routing outputs (any may be null)
+  int32_t* ids_out;
+  uint8_t* expert_class;
+  int32_t* reroute_map;
+  int32_t* active_list;
+  int32_t* n_active;
+  int32_t* status_dev;
+  // align outputs
+  int32_t* plan;
+  int32_t* slot_row;
+  int32_t* row_token;
+  int tiles_gu;      // gate/up units per column block
+  int units_dn_per;  // down units per column block (tiles_dn * ksplit_dn)
+};
+
+struct GemmParams {
+  const uint8_t* a_base;  // bank region: tile (expert, mt, kt) at ((expert*tiles_m+mt)*ktiles+kt)*16KB
+  int tiles_m, ktiles, ksplit;
+  const uint8_t* b_base;  // activations [ktiles][r_max][128 B]
+  int r_max;
+  const int32_t* plan;
+  int Et;
+  int which;  // 0 = gate/up units, 1 = down units
+  int epi, act;
+  uint8_t* h_pack;  // SWIGLU out [d_m_pad/64][r_max][128 B]
+  float* y_perm;    // STORE_F32 out [ksplit][r_max][d_h_pad]
+  int d_h_pad;
+};
+
+cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
+size_t reroute_align_smem(int T, int K, int M, int n_shared);
+cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const __nv_bfloat16* wd, int count,
+                        const Dims& d, int Et, int first, uint8_t* bank, int unpack, cudaStream_t stream);
+cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, const int32_t* row_token,
+                           int r_max, uint8_t* x_pack, int num_sms, cudaStream_t stream);
+cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
+                           const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
+                           __nv_bfloat16* y_bf16, cudaStream_t stream);
+cudaError_t launch_grouped_gemm(const GemmParams& p, int num_sms, cudaStream_t stream);
+size_t grouped_gemm_smem(int Et);
+cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, int T, int d_h, int M, int K,
+                              int32_t* ids, float* weights, float* logits_out, cudaStream_t stream);
+
+}  // namespace sere

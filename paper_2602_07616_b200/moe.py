@@ -1,0 +1,406 @@
+"""GPU-backed mirror of the reference MoE layer path (`sere.moe`).
+
+The reference layer (`/root/reference/pkg/src/sere/moe.py`) is a fp64 numpy
+loop; here one MoE layer is five stream-ordered sm_100a launches behind the
+C-ABI (`sere_layer_forward` / `sere_moe_forward`):
+
+    count/align (+ re-routing)  ->  permute  ->  gate/up tcgen05 GEMM (+SwiGLU)
+    ->  down tcgen05 GEMM  ->  fixed-order combine
+
+Public API, matching the reference names and argument meaning:
+  * `layer_forward(layer, x, assignment, activation)`  drop-in for moe.py:280
+    (host arrays in/out; `layer` a reference MoELayer or an ExpertBank);
+  * `route_topk(router, x)` / `topk_softmax` semantics on the GPU (moe.py:248-277);
+  * `model_forward(model, batch, config, sims, router_override)`  (moe.py:329-377);
+  * device-level: `ExpertBank`, `layer_forward_device`, `moe_forward_device`,
+    `route_topk_device` on CUDA tensors, no host sync.
+Precision: bf16 weights and activations, fp32 accumulation and fp32 layer output
+(SURVEY Appendix B), intermediate h rounded to bf16.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any, Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from . import rerouting as _rr
+from .errors import ConfigError, DimensionError, DomainError, RoutingError, raise_for_status
+
+ACTIVATIONS = ("silu", "relu", "gelu-tanh")
+PHASES = ("prefill", "decode")
+_ACT_CODE = {"silu": 0, "relu": 1, "gelu-tanh": 2}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def activation_code(kind: str) -> int:
+    try:
+        return _ACT_CODE[kind]
+    except KeyError:
+        raise ConfigError(f"unknown activation {kind!r}, expected one of {ACTIVATIONS}") from None
+
+
+def _stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dev_index(device) -> int:
+    torch = _torch()
+    d = torch.device(device)
+    return d.index if d.index is not None else torch.cuda.current_device()
+
+
+# ---------------------------------------------------------------------------
+# expert bank (packed weights of one layer)
+# ---------------------------------------------------------------------------
+
+class ExpertBank:
+    """One layer's routed experts [0,M) and shared experts [M, M+n_shared) as bf16
+    tcgen05 tiles in HBM. Built from reference-orientation weights
+    (ExpertWeights: w_gate/w_up [d_h,d_m], w_down [d_m,d_h]) by `sere_pack_experts`."""
+
+    def __init__(self, n_experts: int, n_shared: int, d_h: int, d_m: int, device=None):
+        torch = _torch()
+        if n_experts < 1 or n_shared < 0 or d_h < 1 or d_m < 1:
+            raise ConfigError("bank needs n_experts >= 1, n_shared >= 0, d_h, d_m >= 1")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        _lib.ensure_device(_dev_index(self.device))
+        self.M, self.n_shared, self.d_h, self.d_m = int(n_experts), int(n_shared), int(d_h), int(d_m)
+        self.n_total = self.M + self.n_shared
+        nbytes = _lib.load().sere_expert_bank_bytes(self.n_total, self.d_h, self.d_m)
+        self.data = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
+    @property
+    def weight_bytes_per_expert(self) -> int:
+        return 2 * 3 * self.d_h * self.d_m
+
+    def pack(self, w_gate, w_up, w_down, first: int = 0, stream=None) -> None:
+        """Pack `count` experts (bf16 CUDA tensors [count,d_h,d_m] x2, [count,d_m,d_h]) into slots first.."""
+        torch = _torch()
+        wg, wu, wd = (t.to(device=self.device, dtype=torch.bfloat16).contiguous() for t in (w_gate, w_up, w_down))
+        count = int(wg.shape[0])
+        if wg.shape != (count, self.d_h, self.d_m) or wu.shape != wg.shape or wd.shape != (count, self.d_m, self.d_h):
+            raise DimensionError("expert weight shapes do not match the bank")
+        _lib.call("sere_pack_experts", wg.data_ptr(), wu.data_ptr(), wd.data_ptr(), count, self.d_h, self.d_m,
+                  self.data.data_ptr(), self.n_total, int(first), _stream_ptr(stream))
+
+    def unpack(self, first: int = 0, count: int | None = None, stream=None):
+        """bf16 (w_gate, w_up, w_down) of bank slots [first, first+count) in the reference orientation."""
+        torch = _torch()
+        count = self.n_total - first if count is None else count
+        wg = torch.empty((count, self.d_h, self.d_m), dtype=torch.bfloat16, device=self.device)
+        wu = torch.empty_like(wg)
+        wd = torch.empty((count, self.d_m, self.d_h), dtype=torch.bfloat16, device=self.device)
+        _lib.call("sere_unpack_experts", self.data.data_ptr(), self.n_total, int(first), int(count), self.d_h,
+                  self.d_m, wg.data_ptr(), wu.data_ptr(), wd.data_ptr(), _stream_ptr(stream))
+        return wg, wu, wd
+
+    @classmethod
+    def from_reference_layer(cls, layer: Any, device=None) -> "ExpertBank":
+        """Convert a reference MoELayer (fp64 numpy ExpertWeights) to a bf16 bank."""
+        torch = _torch()
+        experts = list(layer.experts) + list(getattr(layer, "shared_experts", ()))
+        n_shared = len(getattr(layer, "shared_experts", ()))
+        d_h, d_m = experts[0].w_gate.shape
+        bank = cls(len(experts) - n_shared, n_shared, d_h, d_m, device)
+
+        def stack(name):
+            a = np.stack([np.asarray(getattr(e, name), dtype=np.float32) for e in experts])
+            return torch.from_numpy(a).to(device=bank.device, dtype=torch.bfloat16)
+
+        bank.pack(stack("w_gate"), stack("w_up"), stack("w_down"))
+        return bank
+
+    @classmethod
+    def random(cls, n_experts: int, n_shared: int, d_h: int, d_m: int, seed: int = 0, device=None,
+               keep_raw: bool = False, chunk: int = 16) -> "ExpertBank":
+        """Seeded N(0, 1/d_h) bf16 weights drawn on the device (moe.py:405-413 distribution),
+        generated and packed `chunk` experts at a time so raw weights never all coexist."""
+        torch = _torch()
+        bank = cls(n_experts, n_shared, d_h, d_m, device)
+        gen = torch.Generator(device=bank.device)
+        gen.manual_seed(int(seed))
+        scale = 1.0 / float(np.sqrt(d_h))
+        raw = [] if keep_raw else None
+        for first in range(0, bank.n_total, chunk):
+            c = min(chunk, bank.n_total - first)
+            wg = (torch.randn((c, d_h, d_m), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
+            wu = (torch.randn((c, d_h, d_m), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
+            wd = (torch.randn((c, d_m, d_h), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
+            bank.pack(wg, wu, wd, first)
+            if raw is not None:
+                raw.append((wg, wu, wd))
+        if raw is not None:
+            bank.raw = tuple(torch.cat([r[i] for r in raw]) for i in range(3))
+        return bank
+
+
+# ---------------------------------------------------------------------------
+# workspace cache
+# ---------------------------------------------------------------------------
+
+_WS: dict = {}
+
+
+def workspace(T: int, K: int, M: int, n_shared: int, d_h: int, d_m: int, device) -> Any:
+    torch = _torch()
+    nbytes = _lib.load().sere_layer_workspace_bytes(T, K, M, n_shared, d_h, d_m)
+    key = (str(device),)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+@dataclass
+class LayerOutput:
+    y: Any                  # f32 [T,d_h]
+    y_bf16: Any | None
+    status: Any             # int32 [1]
+    reroute: Any | None = None  # rerouting.DeviceReroute for the fused path
+
+    def check(self) -> None:
+        raise_for_status(int(self.status.item()), "layer")
+
+
+def _check_layer_inputs(bank: ExpertBank, x, ids, weights):
+    torch = _torch()
+    if x.ndim != 2 or x.shape[1] != bank.d_h:
+        raise DimensionError(f"input width {tuple(x.shape)} does not match d_h {bank.d_h}")
+    if ids.ndim != 2 or ids.shape[0] != x.shape[0] or weights.shape != ids.shape:
+        raise DimensionError(f"assignment covers {tuple(ids.shape)} tokens, batch has {x.shape[0]}")
+    if ids.shape[1] > bank.M:
+        raise ConfigError(f"top_k must satisfy 1 <= K <= M (got K={ids.shape[1]}, M={bank.M})")
+    return (x.to(torch.bfloat16).contiguous(), ids.to(torch.int32).contiguous(),
+            weights.to(torch.float32).contiguous())
+
+
+def layer_forward_device(bank: ExpertBank, x, ids, weights, activation: str = "silu", y=None, y_bf16=None,
+                         status=None, stream=None, want_bf16: bool = False) -> LayerOutput:
+    """moe.py:280-310 on CUDA tensors: x bf16 [T,d_h], ids int32 [T,K], weights f32 [T,K]."""
+    torch = _torch()
+    x, ids, weights = _check_layer_inputs(bank, x, ids, weights)
+    T, K = int(ids.shape[0]), int(ids.shape[1])
+    dev = bank.device
+    y = torch.empty((T, bank.d_h), dtype=torch.float32, device=dev) if y is None else y
+    if want_bf16 and y_bf16 is None:
+        y_bf16 = torch.empty((T, bank.d_h), dtype=torch.bfloat16, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev) if status is None else status
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    _lib.call("sere_layer_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
+              activation_code(activation), x.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, y.data_ptr(),
+              y_bf16.data_ptr() if y_bf16 is not None else None, ws.data_ptr(), ws.numel(), status.data_ptr(),
+              _stream_ptr(stream))
+    return LayerOutput(y, y_bf16, status)
+
+
+def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: float, x, ids, weights,
+                       activation: str = "silu", stream=None, want_bf16: bool = False,
+                       out: LayerOutput | None = None) -> LayerOutput:
+    """Fused SERE layer (moe.py:367-375): re-route `ids` against `sim`, then run the
+    layer on the rewritten ids with the ORIGINAL weights (moe.py:369). S == K gives
+    plain top-k on the same kernels."""
+    torch = _torch()
+    cfg = _rr.RerouteConfig(retain_count, threshold)
+    x, ids, weights = _check_layer_inputs(bank, x, ids, weights)
+    T, K = int(ids.shape[0]), int(ids.shape[1])
+    if cfg.retain_count > K:
+        raise ConfigError(f"retain_count must not exceed K (got S={cfg.retain_count}, K={K})")
+    dsim = _rr.as_device_sim(sim, bank.device)
+    if dsim.m != bank.M:
+        raise DimensionError(f"similarity matrix has shape {(dsim.m, dsim.m)}, expected {(bank.M, bank.M)}")
+    dev = bank.device
+    if out is None:
+        rr = _rr.DeviceReroute(
+            new_indices=torch.empty((T, K), dtype=torch.int32, device=dev),
+            expert_class=torch.empty(bank.M, dtype=torch.uint8, device=dev),
+            reroute_map=torch.empty(bank.M, dtype=torch.int32, device=dev),
+            active_list=torch.empty(bank.M, dtype=torch.int32, device=dev),
+            n_active=torch.empty(1, dtype=torch.int32, device=dev),
+            status=torch.zeros(1, dtype=torch.int32, device=dev),
+        )
+        out = LayerOutput(torch.empty((T, bank.d_h), dtype=torch.float32, device=dev),
+                          torch.empty((T, bank.d_h), dtype=torch.bfloat16, device=dev) if want_bf16 else None,
+                          rr.status, rr)
+    rr = out.reroute
+    flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    _lib.call("sere_moe_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
+              activation_code(activation), dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags,
+              x.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, rr.new_indices.data_ptr(),
+              rr.expert_class.data_ptr(), rr.reroute_map.data_ptr(), rr.active_list.data_ptr(),
+              rr.n_active.data_ptr(), out.y.data_ptr(),
+              out.y_bf16.data_ptr() if out.y_bf16 is not None else None, ws.data_ptr(), ws.numel(),
+              out.status.data_ptr(), _stream_ptr(stream))
+    dsim.validated = True
+    return out
+
+
+def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False):
+    """moe.py:268-277 on CUDA: w_router bf16 [d_h,M], x bf16 [T,d_h] -> (ids int32, weights f32[, logits])."""
+    torch = _torch()
+    x = x.to(torch.bfloat16).contiguous()
+    w = w_router.to(torch.bfloat16).contiguous()
+    T, d_h = int(x.shape[0]), int(x.shape[1])
+    if w.shape[0] != d_h:
+        raise DimensionError(f"input width {d_h} does not match router d_h {w.shape[0]}")
+    M = int(w.shape[1])
+    if not 1 <= top_k <= M:
+        raise ConfigError(f"top_k must satisfy 1 <= K <= M (got K={top_k}, M={M})")
+    ids = torch.empty((T, top_k), dtype=torch.int32, device=x.device)
+    wts = torch.empty((T, top_k), dtype=torch.float32, device=x.device)
+    lg = torch.empty((T, M), dtype=torch.float32, device=x.device) if logits else None
+    _lib.call("sere_route_topk", x.data_ptr(), w.data_ptr(), T, d_h, M, int(top_k), ids.data_ptr(),
+              wts.data_ptr(), lg.data_ptr() if lg is not None else None, _stream_ptr(stream))
+    return (ids, wts, lg) if logits else (ids, wts)
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped drop-ins (host arrays in/out)
+# ---------------------------------------------------------------------------
+
+_BANKS: dict[int, tuple[Any, ExpertBank]] = {}
+
+
+def bank_for(layer: Any) -> ExpertBank:
+    """ExpertBank of a reference MoELayer, converted once and cached by identity."""
+    if isinstance(layer, ExpertBank):
+        return layer
+    hit = _BANKS.get(id(layer))
+    if hit is not None and hit[0] is layer:
+        return hit[1]
+    bank = ExpertBank.from_reference_layer(layer)
+    if len(_BANKS) > 256:
+        _BANKS.clear()
+    _BANKS[id(layer)] = (layer, bank)
+    return bank
+
+
+def layer_forward(layer: Any, x: Any, assignment: Any, activation: str = "silu") -> np.ndarray:
+    """Drop-in for moe.layer_forward (moe.py:280-310): weighted sum of routed experts in
+    slot order plus every shared expert, on the GPU. Returns float64 [T,d_h] (the fp32
+    device result widened)."""
+    torch = _torch()
+    activation_code(activation)
+    bank = bank_for(layer)
+    xa = np.asarray(x, dtype=np.float64)
+    if xa.ndim != 2:
+        raise DimensionError(f"x must be 2-D, got shape {xa.shape}")
+    idx = np.asarray(assignment.indices)
+    w = np.asarray(assignment.weights, dtype=np.float64)
+    if idx.shape[0] != xa.shape[0]:
+        raise DimensionError(f"assignment covers {idx.shape[0]} tokens, batch has {xa.shape[0]}")
+    if xa.shape[1] != bank.d_h:
+        raise DimensionError(f"input width {xa.shape[1]} does not match expert d_h {bank.d_h}")
+    if not np.all(np.isfinite(xa)):
+        raise DomainError("expert input contains non-finite values")
+    if idx.size and (idx.min() < 0 or idx.max() >= bank.M):
+        raise RoutingError(f"assignment refers to experts outside [0, {bank.M})")
+    dev = bank.device
+    out = layer_forward_device(bank, torch.from_numpy(xa).to(dev), torch.from_numpy(idx.astype(np.int32)).to(dev),
+                               torch.from_numpy(w.astype(np.float32)).to(dev), activation)
+    out.check()
+    return out.y.double().cpu().numpy()
+
+
+@dataclass
+class LayerTrace:
+    """moe.py:313-320."""
+
+    original: Any
+    final: Any
+    reroute: Any
+    active: frozenset
+
+
+@dataclass
+class ForwardResult:
+    """moe.py:323-326."""
+
+    output: np.ndarray
+    layers: list = field(default_factory=list)
+
+
+@dataclass
+class Assignment:
+    """Host twin of RoutingAssignment (moe.py:193-232) used in traces."""
+
+    indices: np.ndarray
+    weights: np.ndarray
+
+    @property
+    def n_tokens(self) -> int:
+        return self.indices.shape[0]
+
+    @property
+    def top_k(self) -> int:
+        return self.indices.shape[1]
+
+
+def route_topk(router: Any, x: Any) -> Assignment:
+    """moe.py:268-277 on the GPU for a reference RouterWeights (bf16 weights, fp32 logits)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    w = torch.as_tensor(np.asarray(router.w_router, dtype=np.float32)).to(dev)
+    xt = torch.as_tensor(np.asarray(x, dtype=np.float32)).to(dev)
+    ids, wts = route_topk_device(w, xt, int(router.top_k))
+    return Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
+
+
+def model_forward(model: Any, batch: Any, config: Any = None, sims: Sequence | None = None,
+                  router_override: Callable | None = None) -> ForwardResult:
+    """moe.py:329-377 with every layer on the GPU: route -> (phase-gated) fused
+    re-route + layer. Routing uses the GPU router unless `router_override` is given."""
+    torch = _torch()
+    x_np = np.asarray(batch.x, dtype=np.float64)
+    if x_np.shape[1] != model.d_h:
+        raise DimensionError(f"batch width {x_np.shape[1]} does not match model d_h {model.d_h}")
+    if config is not None:
+        if sims is None or len(sims) != model.n_layers:
+            raise DimensionError(f"rewriting needs one similarity matrix per layer ({model.n_layers})")
+        for l, sim in enumerate(sims):
+            m = model.layers[l].n_experts
+            if np.shape(getattr(sim, "values", sim)) != (m, m):
+                raise DimensionError(f"similarity matrix for layer {l} has wrong shape, expected {(m, m)}")
+    apply_rewrite = config is not None and (config.phase_mode == "all_phases" or batch.phase == "decode")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.from_numpy(x_np).to(dev)
+    traces = []
+    for l, layer in enumerate(model.layers):
+        bank = bank_for(layer)
+        if router_override is not None:
+            a = router_override(l, x.double().cpu().numpy())
+            ids = torch.as_tensor(np.asarray(a.indices).astype(np.int32)).to(dev)
+            wts = torch.as_tensor(np.asarray(a.weights, dtype=np.float32)).to(dev)
+            original = a
+        else:
+            wr = torch.as_tensor(np.asarray(layer.router.w_router, dtype=np.float32)).to(dev)
+            ids, wts = route_topk_device(wr, x, int(layer.router.top_k))
+            original = Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
+        if apply_rewrite:
+            dsim = _rr._cached_sim(sims[l], dev)
+            out = moe_forward_device(bank, dsim, config.retain_count, config.threshold, x, ids, wts,
+                                     model.activation)
+            out.check()
+            res = out.reroute.to_result()
+            final = Assignment(res.new_indices, np.asarray(original.weights, dtype=np.float64))
+            active = res.final_active
+        else:
+            out = layer_forward_device(bank, x, ids, wts, model.activation)
+            out.check()
+            res = None
+            final = original
+            active = frozenset(np.unique(np.asarray(original.indices)).tolist())
+        x = out.y
+        traces.append(LayerTrace(original=original, final=final, reroute=res, active=active))
+    return ForwardResult(output=x.double().cpu().numpy(), layers=traces)

@@ -1,0 +1,97 @@
+import json
+import os
+import pathlib
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
+
+try:  # derandomized hypothesis, as the reference suite does (tests/conftest.py:9-15 there)
+    from hypothesis import HealthCheck, settings
+
+    settings.register_profile("repo", derandomize=True, deadline=None,
+                              suppress_health_check=[HealthCheck.too_slow])
+    settings.load_profile("repo")
+except ImportError:  # pragma: no cover
+    pass
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
+
+
+def pytest_collection_modifyitems(config, items):
+    # A `-m gpu` run on a box without a GPU should fail loudly, never silently skip.
+    pass
+
+
+class RerouteGoldens:
+    """Reader for tests/golden/reroute_cases.npz (written by make_golden.py)."""
+
+    def __init__(self, path=GOLDEN / "reroute_cases.npz"):
+        z = np.load(path, allow_pickle=False)
+        self.z = z
+        self.sets = json.loads(str(z["sets_json"]))
+        self.n = len(self.sets)
+
+    def _get(self, prefix, i):
+        z = self.z
+        off = z[prefix + "_off"]
+        shape = tuple(z[prefix + "_shape"][i])
+        return z[prefix + "_flat"][off[i]:off[i + 1]].reshape(shape)
+
+    def case(self, i):
+        from oracle.sere_oracle import random_symmetric_sim
+
+        z = self.z
+        seed = int(z["sim_seed"][i])
+        m = int(z["m"][i])
+        if seed >= 0:
+            sim = random_symmetric_sim(np.random.default_rng(seed), m)
+        else:
+            sim = self._get("sim", i)
+        s = self.sets[i]
+        return dict(
+            ids_in=self._get("ids_in", i),
+            ids_out=self._get("ids_out", i),
+            sim=sim,
+            retain=int(z["retain"][i]),
+            rho=float(z["rho"][i]),
+            source=str(z["source"][i]),
+            primary=frozenset(s["primary"]),
+            critical=frozenset(s["critical"]),
+            active=frozenset(s["active"]),
+            map={int(u): int(v) for u, v in s["map"].items()},
+        )
+
+    def __iter__(self):
+        for i in range(self.n):
+            yield self.case(i)
+
+
+@pytest.fixture(scope="session")
+def reroute_goldens():
+    return RerouteGoldens()
+
+
+@pytest.fixture(scope="session")
+def layer_goldens():
+    z = np.load(GOLDEN / "layer_cases.npz", allow_pickle=False)
+    return z, json.loads(str(z["configs_json"]))
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    """The GPU tests' device; fails (not skips) when the box has no usable GPU."""
+    import torch
+
+    assert torch.cuda.is_available(), "gpu-marked test needs a CUDA device"
+    major, minor = torch.cuda.get_device_capability(0)
+    assert (major, minor) == (10, 0), f"expected sm_100 (B200), got sm_{major}{minor}"
+    return torch.device("cuda", 0)

@@ -1,0 +1,117 @@
+"""CPU-only checks of the C-ABI library: it loads, exports exactly what include/sere_b200.h
+declares, and its host-side functions (sizes, layouts, status strings, config checks) behave.
+No kernel is launched here."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "sere_b200.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2602_07616_b200 import _lib, build
+
+    build.build()
+    return _lib.load()
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sere_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree(lib):
+    from paper_2602_07616_b200 import _lib
+
+    decl = declared_functions()
+    assert len(decl) >= 12
+    assert sorted(_lib.SIGNATURES) == decl
+    for name in decl:
+        assert hasattr(lib, name), name  # exported from the .so
+
+
+def test_exports_are_extern_c(lib):
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", str(ROOT / "paper_2602_07616_b200" / "libsere_b200.so")],
+                         capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (sere_\w+)", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_host_side_functions(lib):
+    from paper_2602_07616_b200 import _lib
+
+    assert lib.sere_abi_version() == 1
+    assert lib.sere_status_string(1) == b"ConfigError"
+    assert lib.sere_status_string(4) == b"RoutingError"
+    # bank bytes = E * 3 * d_h_pad * d_m_pad * 2 (bf16)
+    assert lib.sere_expert_bank_bytes(128, 2048, 768) == 128 * 3 * 2048 * 768 * 2
+    assert lib.sere_expert_bank_bytes(8, 4096, 14336) == 8 * 3 * 4096 * 14336 * 2
+    assert lib.sere_expert_bank_bytes(5, 24, 40) == 5 * 3 * 128 * 64 * 2  # padded to 128 / 64
+    L = _lib.workspace_layout(512, 8, 128, 0, 2048, 768)
+    assert L.r_max >= 512 * 8 + 16 * 128 and L.r_max % 8 == 0
+    assert L.d_h_pad == 2048 and L.d_m_pad == 768 and L.ksplit_down == 1
+    assert L.off_x_pack % 1024 == 0 and L.off_h_pack % 1024 == 0 and L.off_y_perm % 1024 == 0
+    assert lib.sere_layer_workspace_bytes(512, 8, 128, 0, 2048, 768) == L.total_bytes
+    Lm = _lib.workspace_layout(256, 2, 8, 0, 4096, 14336)
+    assert Lm.ksplit_down == 7  # 224 K-tiles of the down GEMM split 7 ways
+
+
+def test_host_config_checks_without_gpu(lib):
+    from paper_2602_07616_b200.errors import SERE_ERR_CONFIG, SERE_ERR_DIMENSION, SERE_ERR_UNSUPPORTED
+
+    p = ctypes.c_void_p(16)
+    # S > K -> ConfigError (rerouting.py:104-107); rho outside [0,1] -> ConfigError; S < 1
+    assert lib.sere_reroute(p, p, 4, 2, 8, 3, 0.5, 0, p, p, p, p, p, p, None) == SERE_ERR_CONFIG
+    assert lib.sere_reroute(p, p, 4, 2, 8, 1, 1.5, 0, p, p, p, p, p, p, None) == SERE_ERR_CONFIG
+    assert lib.sere_reroute(p, p, 4, 2, 8, 0, 0.5, 0, p, p, p, p, p, p, None) == SERE_ERR_CONFIG
+    assert lib.sere_reroute(p, p, 4, 2, 8, 1, float("nan"), 0, p, p, p, p, p, p, None) == SERE_ERR_CONFIG
+    assert lib.sere_reroute(p, p, 4, 0, 8, 1, 0.5, 0, p, p, p, p, p, p, None) == SERE_ERR_DIMENSION
+    assert lib.sere_reroute(p, p, 8192, 4, 8, 1, 0.5, 0, p, p, p, p, p, p, None) == SERE_ERR_UNSUPPORTED
+    # K > M is a ConfigError (moe.py:116-118); workspace too small is reported, never overrun
+    assert lib.sere_layer_forward(p, 4, 0, 128, 64, 0, p, p, p, 2, 8, p, None, p, 1 << 30, p, None) == SERE_ERR_CONFIG
+    from paper_2602_07616_b200.errors import SERE_ERR_WORKSPACE
+
+    assert lib.sere_layer_forward(p, 8, 0, 128, 64, 0, p, p, p, 2, 2, p, None, p, 16, p, None) == SERE_ERR_WORKSPACE
+    assert lib.sere_device_check(0) != 0  # no GPU in this container
+
+
+def test_errors_map_one_to_one():
+    from paper_2602_07616_b200 import errors as E
+
+    assert E.exception_for_status(0) is None
+    assert isinstance(E.exception_for_status(E.SERE_ERR_CONFIG), E.ConfigError)
+    assert isinstance(E.exception_for_status(E.SERE_ERR_DIMENSION), E.DimensionError)
+    assert isinstance(E.exception_for_status(E.SERE_ERR_INPUT), E.InputError)
+    assert isinstance(E.exception_for_status(E.SERE_ERR_ROUTING), E.RoutingError)
+    assert isinstance(E.exception_for_status(E.SERE_ERR_DOMAIN), E.DomainError)
+    for code in range(1, 9):
+        assert isinstance(E.exception_for_status(code), E.SereError)
+
+
+def test_python_config_mirror():
+    from paper_2602_07616_b200.errors import ConfigError
+    from paper_2602_07616_b200.rerouting import RerouteConfig
+
+    c = RerouteConfig(retain_count=2.0, threshold=1)
+    assert c.retain_count == 2 and isinstance(c.retain_count, int) and c.threshold == 1.0
+    for bad in (dict(retain_count=0, threshold=0.5), dict(retain_count=1, threshold=-0.1),
+                dict(retain_count=1, threshold=0.5, phase_mode="prefill_only")):
+        with pytest.raises(ConfigError):
+            RerouteConfig(**bad)
+
+
+def test_product_never_imports_oracle():
+    """The product package must not route through the CPU oracle."""
+    pkg = ROOT / "paper_2602_07616_b200"
+    for p in pkg.rglob("*.py"):
+        src = p.read_text()
+        assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+([\w\.]+)", src, flags=re.M), p
+        assert "sere_oracle" not in src, p
