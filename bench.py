@@ -1,0 +1,500 @@
+#!/usr/bin/env python
+"""bench.py -- SERE batched-decode MoE on B200 (driver contract, one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (expert-parallel, NCCL)
+
+Workload (default, every N): BASELINE configs[4] -- the Qwen3-30B-A3B 48-layer MoE
+decode step, T = 512 tokens, M = 128 experts, top-8, d_h = 2048, d_m = 768, bf16,
+expert-parallel over N GPUs (experts split, token slices, all-gather / reduce-scatter
+over NCCL). It is the only BASELINE config defined at 1/2/4/8 GPUs, so the driver's
+per-N values compare the same work (strong scaling). One "step" = one decode step of
+all 48 layers (router -> SERE re-routing -> grouped FFN) for the 512 tokens.
+`value` = SERE decode tokens/s with inputs resident in HBM (CUDA-graph replay,
+CUDA events, max over ranks); the same step with plain top-k on the same kernels,
+the re-routing kernel time and the grouped FFN's HBM roofline are reported beside it.
+Weights are random N(0, 1/d_h) (no checkpoints offline); expert weights (58 GB) far
+exceed the 126 MB L2, so no flush is needed between steps.
+
+--impl reference: the reference CPU algorithm (the numpy oracle port of
+sere.moe.model_forward's per-layer body: fp64 route_topk + apply_sere + layer_forward)
+on the host cores, same config and metric; each step is one of the 48 layers,
+extrapolated x48 (a full fp64 step needs 232 GB).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE decode tokens/s SERE vs top-k; reroute kernel µs; expert-FFN HBM GB/s"
+
+WORKLOADS = {
+    "c4": dict(name="qwen3-30b-a3b-moe-decode-48L", M=128, K=8, d_h=2048, d_m=768, n_shared=0, L=48, T=512),
+    "c2": dict(name="qwen3-30b-a3b-moe-layer", M=128, K=8, d_h=2048, d_m=768, n_shared=0, L=1, T=128),
+    "c3": dict(name="deepseek-v2-lite-moe-layer", M=64, K=6, d_h=2048, d_m=1408, n_shared=2, L=1, T=256),
+    "c1": dict(name="mixtral-8x7b-moe-layer", M=8, K=2, d_h=4096, d_m=14336, n_shared=0, L=1, T=256),
+    "c0": dict(name="toy-moe-layer", M=8, K=2, d_h=256, d_m=512, n_shared=0, L=1, T=16),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--T", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--retain", type=int, default=1)
+    ap.add_argument("--threshold", type=float, default=0.5)
+    ap.add_argument("--beta", type=float, default=1.0, help="router popularity skew (SURVEY Appendix C)")
+    ap.add_argument("--sim", choices=["uniform", "clustered"], default="uniform")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    a = ap.parse_args()
+    wl = dict(WORKLOADS[a.workload])
+    if a.T:
+        wl["T"] = a.T
+    if a.layers:
+        wl["L"] = a.layers
+    return a, wl
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def host_info():
+    import platform
+
+    cores = os.cpu_count() or 1
+    model = platform.processor() or ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas_threads = cores
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        if info:
+            blas_threads = max(int(i.get("num_threads", 1)) for i in info)
+    except Exception:
+        pass
+    return cores, model, blas_threads
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling through NVML, every 20 ms, during the timed regions."""
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._on = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        if not self.ok:
+            return
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            if self._on.is_set():
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                    for bit, name in names.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(0.02)
+
+    def start(self):
+        self._on.set()
+
+    def pause(self):
+        self._on.clear()
+
+    def close(self):
+        self._stop.set()
+        self.t.join(timeout=1)
+
+    def summary(self):
+        import statistics
+
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+# --------------------------------------------------------------------------- timing
+def time_region(torch, fn, steps, world, sync_group=None):
+    """barrier + sync, CUDA events around `steps` calls on the current stream, barrier + sync;
+    returns ms per step, max over ranks."""
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = s.elapsed_time(e) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def algorithmic_bytes(wl, n_active, T):
+    """bytes per MoE layer x decode step of T tokens."""
+    return (2 * 3 * wl["d_h"] * wl["d_m"] * (n_active + wl["n_shared"]) + 2 * T * wl["d_h"] + 4 * T * wl["d_h"]
+            + 8 * T * wl["K"])
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_layer_sample(wl, layer_np, h, sim, S, rho, bias, seconds):
+    """Time the reference per-layer body (fp64) on one layer: route + apply_sere + layer_forward."""
+    import numpy as np
+
+    from oracle import sere_oracle as O
+
+    def once():
+        logits = h @ layer_np.w_router + bias[None, :]
+        ids, w = O.topk_softmax(logits, wl["K"])
+        res = O.apply_sere(ids, sim, S, rho)
+        return O.layer_forward(layer_np, h, res.new_indices, w)
+
+    once()  # numpy / BLAS warm-up
+    times = []
+    t_end = time.perf_counter() + seconds
+    while len(times) < 2 or (time.perf_counter() < t_end and len(times) < 10):
+        t0 = time.perf_counter()
+        once()
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), len(times)
+
+
+def oracle_layer_from_bank(torch, model, l):
+    """Layer l of the device model as an fp64 oracle layer (same bf16 values)."""
+    import numpy as np
+
+    from oracle import sere_oracle as O
+
+    layer = model.layers[l]
+    wg, wu, wd = layer.bank.unpack()
+    experts = []
+    for e in range(wg.shape[0]):
+        experts.append(O.OracleExpert(wg[e].double().cpu().numpy(), wu[e].double().cpu().numpy(),
+                                      wd[e].double().cpu().numpy()))
+    del wg, wu, wd
+    torch.cuda.empty_cache()
+    n_r = model.M
+    return O.OracleLayer(experts[:n_r], layer.w_router.double().cpu().numpy(), model.K, experts[n_r:])
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, wl):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_env()
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2602_07616_b200 import build as _build
+
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    from paper_2602_07616_b200 import decode, ep
+
+    T, L = wl["T"], wl["L"]
+    if world > 1:
+        lo, hi = ep.expert_range(wl["M"], world, rank)
+        shard = dict(expert_ids=list(range(lo, hi)), shared_ids=ep.shared_owned(wl["n_shared"], world, rank))
+    else:
+        lo, hi = 0, wl["M"]
+        shard = {}
+    t_build = time.perf_counter()
+    model = decode.DecodeModel(L, wl["M"], wl["K"], wl["d_h"], wl["d_m"], wl["n_shared"], seed=0, beta=args.beta,
+                               sim_kind=args.sim, **shard)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+
+    def make_step(mode):
+        if world > 1:
+            return ep.EPDecodeStep(model, T, args.retain, args.threshold, mode)
+        return decode.DecodeStep(model, T, args.retain, args.threshold, mode)
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1)
+    x_full = torch.randn((T, wl["d_h"]), generator=gen, device="cuda")
+    sere = make_step("sere")
+    topk = make_step("topk")
+    t_local = sere.T_local if world > 1 else T
+    x_local = x_full[rank * t_local:(rank + 1) * t_local].contiguous()
+    sere.x_in.copy_(x_local)
+    topk.x_in.copy_(x_local)
+    graphed = []
+    for st in (sere, topk):
+        ok = st.capture()
+        graphed.append(True if ok is None else bool(ok))
+
+    clocks = ClockSampler(local)
+    for _ in range(args.warmup):
+        sere.run()
+        topk.run()
+    torch.cuda.synchronize()
+    sere.check()
+    topk.check()
+
+    clocks.start()
+    ms_sere = time_region(torch, sere.run, args.steps, world)
+    ms_topk = time_region(torch, topk.run, args.steps, world)
+    # end-to-end through the public call: pinned host x -> step -> pinned host result
+    x_host = x_local.cpu().pin_memory()
+    out_host = torch.empty_like(x_host).pin_memory()
+    for _ in range(2):
+        sere.run_host(x_host, out_host)
+    ms_e2e = time_region(torch, lambda: sere.run_host(x_host, out_host), args.steps, world)
+    clocks.pause()
+    sere.check()
+
+    act_sere = sere.active_counts().astype(float)
+    act_topk = topk.active_counts().astype(float)
+
+    # ---- roofline pass: the same SERE step with per-stage CUDA events captured in its graph
+    prof = make_step("sere")
+    prof.x_in.copy_(x_local)
+    prof.enable_stage_events()
+    roof = None
+    reroute_us = None
+    if getattr(prof, "stage_events", None) is not None:
+        prof.capture()
+        for _ in range(3):
+            prof.run()
+        torch.cuda.synchronize()
+        st = prof.stage_times_ms()  # [L, 5]
+        acts = prof.active_counts()
+        if world > 1:
+            cls = [o.reroute.expert_class[lo:hi].cpu().numpy() for o in prof.outs]
+            acts_local = np.array([int(((c & 3) != 0).sum()) for c in cls], dtype=float)
+        else:
+            acts_local = acts.astype(float)
+        ffn_ms = st[:, 2] + st[:, 3]
+        n_sh_local = len(model.shared_ids)
+        wl_local = dict(wl, n_shared=n_sh_local)
+        bytes_layers = np.array([algorithmic_bytes(wl_local, a, T) for a in acts_local], dtype=float)
+        achieved = float(bytes_layers.sum() / (ffn_ms.sum() * 1e-3) / 1e9)
+        peak, peak_kind = measured_peak_hbm()
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "grouped_gemm_kernel (gate/up + down launches, tcgen05)",
+                "peak_kind": peak_kind,
+                "bytes_per_layer_avg": float(bytes_layers.mean()),
+                "ffn_us_per_layer_avg": float(ffn_ms.mean() * 1e3),
+                "stage_us_per_layer_avg": {k: round(float(v) * 1e3, 2) for k, v in
+                                           zip(["reroute_align", "permute", "gate_up_gemm", "down_gemm", "combine"],
+                                               st.mean(axis=0))},
+                "ffn_share_of_layer_kernels": round(float(ffn_ms.sum() / st.sum()), 4)}
+        reroute_us = round(float(st[:, 0].mean() * 1e3), 2)
+        del prof
+    clocks.close()
+
+    # ---- CPU baseline: rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores, cpu_model, blas = host_info()
+        try:
+            layer_np = oracle_layer_from_bank(torch, model, 0)
+            h0 = torch.nn.functional.rms_norm(x_full, (wl["d_h"],), eps=1e-6).to(torch.bfloat16).double().cpu().numpy()
+            sim0 = model.sims_host[0]
+            bias0 = model.layers[0].bias.double().cpu().numpy()
+            t_layer, n = cpu_layer_sample(wl, layer_np, h0, sim0, args.retain, args.threshold, bias0,
+                                          args.cpu_seconds)
+            cpu = {"value": round(T / (t_layer * L), 3), "unit": "tokens/s", "cores": blas, "kind": "port",
+                   "sample": f"1 of {L} layers (fp64 route_topk + apply_sere + layer_forward, T={T}), "
+                             f"median of {n} runs = {t_layer * 1e3:.1f} ms, extrapolated x{L}",
+                   "cpu_model": cpu_model, "host_cores": cores}
+            del layer_np
+        except MemoryError as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "port", "sample": f"skipped: {exc}"}
+
+    tok_s = T / (ms_sere * 1e-3)
+    tok_s_topk = T / (ms_topk * 1e-3)
+    line = {
+        "metric": METRIC,
+        "value": round(tok_s, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_sere, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: random N(0,1/d_h) bf16 expert/router weights, N(0,1) token states, "
+                "uniform symmetric similarity (reference test construction), router skew beta",
+        "config": {"workload": wl["name"], "global_batch": T, "layers": L, "experts": wl["M"], "top_k": wl["K"],
+                   "d_h": wl["d_h"], "d_m": wl["d_m"], "shared_experts": wl["n_shared"],
+                   "retain_S": args.retain, "threshold_rho": args.threshold, "router_skew_beta": args.beta,
+                   "sim": args.sim, "block": "prenorm_residual (RMSNorm -> router -> SERE -> grouped FFN -> +x)",
+                   "parallelism": f"ep{world}", "l2": "no flush: 58 GB of expert weights per step >> 126 MB L2",
+                   "cuda_graph": all(graphed)},
+        "topk": {"value": round(tok_s_topk, 1), "unit": "tokens/s", "ms_per_step": round(ms_topk, 4),
+                 "active_experts_per_layer": round(float(act_topk.mean()), 2)},
+        "sere": {"active_experts_per_layer": round(float(act_sere.mean()), 2),
+                 "weight_bytes_skipped_frac": round(1.0 - float(act_sere.sum() / max(act_topk.sum(), 1)), 4),
+                 "speedup_vs_topk": round(ms_topk / ms_sere, 4)},
+        "reroute_kernel_us": reroute_us,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(T / (ms_e2e * 1e-3), 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
+                "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": int(sere.launches_per_step * args.steps),
+        "clocks": clocks.summary(),
+        "setup_s": round(t_build, 1),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, wl):
+    import numpy as np
+
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import sere_oracle as O
+    from paper_2602_07616_b200.decode import clustered_sim, uniform_sim
+
+    T, L, M, K, d_h, d_m, ns = wl["T"], wl["L"], wl["M"], wl["K"], wl["d_h"], wl["d_m"], wl["n_shared"]
+    rng = np.random.default_rng(0)
+    scale = 1.0 / np.sqrt(d_h)
+
+    def draw(shape):
+        return (rng.standard_normal(shape, dtype=np.float32) * np.float32(scale)).astype(np.float64)
+
+    experts = [O.OracleExpert(draw((d_h, d_m)), draw((d_h, d_m)), draw((d_m, d_h))) for _ in range(M + ns)]
+    layer = O.OracleLayer(experts[:M], draw((d_h, M)), K, experts[M:])
+    bias = args.beta * rng.standard_normal(M)
+    sim = clustered_sim(rng, M) if args.sim == "clustered" else uniform_sim(rng, M)
+    x = rng.standard_normal((T, d_h))
+    h = x / np.sqrt((x * x).mean(axis=1, keepdims=True) + 1e-6)
+
+    def sample():
+        logits = h @ layer.w_router + bias[None, :]
+        ids, w = O.topk_softmax(logits, K)
+        res = O.apply_sere(ids, sim, args.retain, args.threshold)
+        return O.layer_forward(layer, h, res.new_indices, w)
+
+    for _ in range(args.warmup):
+        sample()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sample()
+    t_layer = (time.perf_counter() - t0) / args.steps
+    ms_step = t_layer * L * 1e3
+    value = T / (ms_step * 1e-3)
+    cores, cpu_model, blas = host_info()
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, same shapes/distributions as the ours arm",
+        "config": {"workload": wl["name"], "global_batch": T, "layers": L, "experts": M, "top_k": K, "d_h": d_h,
+                   "d_m": d_m, "shared_experts": ns, "retain_S": args.retain, "threshold_rho": args.threshold,
+                   "router_skew_beta": args.beta, "sim": args.sim, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": blas, "kind": "port",
+                         "sample": f"each step = 1 of {L} layers (fp64 oracle port of the reference per-layer "
+                                   f"body), extrapolated x{L}", "cpu_model": cpu_model, "host_cores": cores},
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args, wl = parse_args()
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

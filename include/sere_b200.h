@@ -136,12 +136,44 @@ int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, in
                      size_t workspace_bytes, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------
+ * (4b) Expert-parallel shard of (4): the bank holds only global experts
+ *     [expert_lo, expert_hi) (as bank slots 0..) plus n_shared_local shared
+ *     experts. Re-routing runs on the FULL gathered [T,K] table (every rank
+ *     computes the same bit-exact ids), then only this rank's experts are
+ *     evaluated; y_partial [T,d_h] f32 = this rank's share of moe.layer_forward's
+ *     sum (slot order kept). Ranks' partials are summed by the caller's
+ *     reduce-scatter (paper_2602_07616_b200/ep.py). Workspace: size it with
+ *     sere_layer_workspace_bytes(T, K, expert_hi-expert_lo, n_shared_local, ...).
+ * ------------------------------------------------------------------------ */
+int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, int n_shared_local, int d_h,
+                        int d_m, int activation, const double* sim, int S, double rho, int flags,
+                        const uint16_t* x, const int32_t* ids_in, const float* weights, int T, int K,
+                        int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map,
+                        int32_t* active_list, int32_t* n_active, float* y_partial, void* workspace,
+                        size_t workspace_bytes, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
  * (5) Router: logits = x W_r (fp32 accumulate), top-K with ties to the lower
  *     index, softmax over the K picks.  Replaces moe.route_topk / topk_softmax
  *     (moe.py:248-277).  w_router bf16 [d_h, M] (reference orientation).
  * ------------------------------------------------------------------------ */
-int sere_route_topk(const uint16_t* x, const uint16_t* w_router, int T, int d_h, int M, int K,
-                    int32_t* ids, float* weights, float* logits_out, void* stream);
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router, const float* bias, int T, int d_h, int M,
+                    int K, int32_t* ids, float* weights, float* logits_out, void* stream);
+/*   bias f32 [M] (nullable) is added to the logits before selection: the benchmark's
+ *   expert-popularity skew knob; NULL reproduces moe.route_topk.      */
+
+/* ------------------------------------------------------------------------
+ * (6) Decode-block glue: x += y (fp32 residual stream, y nullable) and
+ *     h = bf16(x * rsqrt(mean(x^2) + eps)) -- the pre-norm of a Qwen3-style MoE block
+ *     used by the 48-layer benchmark step (not part of the reference model).
+ * ------------------------------------------------------------------------ */
+int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int d_h, float eps, void* stream);
+
+/* Profiling hook: when n == 6, every following layer call on this host thread records
+ * events[0..4] before its five stages (align, permute, gate/up GEMM, down GEMM,
+ * combine) and events[5] after the last, on the launch stream (cudaEvent_t handles).
+ * n == 0 disables. */
+int sere_set_stage_events(void* const* events, int n);
 
 /* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).

@@ -34,6 +34,14 @@ int num_sms() {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+constexpr int kStageEvents = 6;
+thread_local cudaEvent_t t_stage_events[kStageEvents];
+thread_local bool t_stage_events_on = false;
+
+inline void stage_mark(int i, cudaStream_t stream) {
+  if (t_stage_events_on) cudaEventRecord(t_stage_events[i], stream);
+}
+
 struct WsLayout {
   size_t plan, slot_row, row_token, x_pack, h_pack, y_perm, total;
   int r_max;
@@ -84,12 +92,14 @@ int check_reroute_cfg(int K, int M, int S, double rho) {
   return SERE_OK;
 }
 
-int run_layer(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, const double* sim, int S,
+// M = global expert count; the bank holds global experts [e_lo, e_lo + m_local) + n_shared shared ones
+int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int d_h, int d_m, int activation,
+              const double* sim, int S,
               double rho, int flags, int mode, const uint16_t* x, const int32_t* ids_in, const float* weights,
               int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
               int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
               int32_t* status_dev, cudaStream_t stream) {
-  const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
+  const WsLayout L = ws_layout(T, K, m_local, n_shared, d_h, d_m);
   if (workspace == nullptr || workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
   if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr || y == nullptr)
     return SERE_ERR_DIMENSION;
@@ -121,9 +131,13 @@ int run_layer(const void* bank, int M, int n_shared, int d_h, int d_m, int activ
   ap.row_token = row_token;
   ap.tiles_gu = d.tiles_gu;
   ap.units_dn_per = d.tiles_dn * d.ksplit_dn;
+  ap.e_lo = e_lo;
+  ap.m_local = m_local;
+  stage_mark(0, stream);
   cudaError_t e = launch_reroute_align(ap, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
+  stage_mark(1, stream);
   e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
@@ -144,6 +158,7 @@ int run_layer(const void* bank, int M, int n_shared, int d_h, int d_m, int activ
   gp.h_pack = h_pack;
   gp.y_perm = y_perm;
   gp.d_h_pad = d.d_h_pad;
+  stage_mark(2, stream);
   e = launch_grouped_gemm(gp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
@@ -154,11 +169,14 @@ int run_layer(const void* bank, int M, int n_shared, int d_h, int d_m, int activ
   gp.b_base = h_pack;
   gp.which = 1;
   gp.epi = 1;
+  stage_mark(3, stream);
   e = launch_grouped_gemm(gp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
+  stage_mark(4, stream);
   e = launch_combine(y_perm, d, L.r_max, plan, slot_row, weights, T, K, n_shared, y,
                      reinterpret_cast<__nv_bfloat16*>(y_bf16), stream);
+  stage_mark(5, stream);
   return check_cuda(e);
 }
 
@@ -208,6 +226,8 @@ int sere_reroute(const int32_t* ids_in, const double* sim, int T, int K, int M, 
   ap.rho = rho;
   ap.flags = flags;
   ap.mode = MODE_REROUTE;
+  ap.e_lo = 0;
+  ap.m_local = M;
   ap.ids_out = ids_out;
   ap.expert_class = expert_class;
   ap.reroute_map = reroute_map;
@@ -282,7 +302,8 @@ int sere_layer_forward(const void* bank, int M, int n_shared, int d_h, int d_m, 
   const int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
   if (rc != SERE_OK) return rc;
   if (T == 0) return SERE_OK;
-  return run_layer(bank, M, n_shared, d_h, d_m, activation, nullptr, K, 0.0, 0, MODE_ALIGN, x, ids, weights, T, K,
+  return run_layer(bank, M, 0, M, n_shared, d_h, d_m, activation, nullptr, K, 0.0, 0, MODE_ALIGN, x, ids, weights,
+                   T, K,
                    nullptr, nullptr, nullptr, nullptr, nullptr, y, y_bf16, workspace, workspace_bytes, status_dev,
                    static_cast<cudaStream_t>(stream));
 }
@@ -298,20 +319,60 @@ int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, in
   if (rc != SERE_OK) return rc;
   if (sim == nullptr) return SERE_ERR_DIMENSION;
   if (T == 0) return SERE_OK;
-  return run_layer(bank, M, n_shared, d_h, d_m, activation, sim, S, rho, flags, MODE_REROUTE | MODE_ALIGN, x,
+  return run_layer(bank, M, 0, M, n_shared, d_h, d_m, activation, sim, S, rho, flags, MODE_REROUTE | MODE_ALIGN, x,
                    ids_in, weights, T, K, ids_out, expert_class, reroute_map, active_list, n_active, y, y_bf16,
                    workspace, workspace_bytes, status_dev, static_cast<cudaStream_t>(stream));
 }
 
-int sere_route_topk(const uint16_t* x, const uint16_t* w_router, int T, int d_h, int M, int K, int32_t* ids,
-                    float* weights, float* logits_out, void* stream) {
+int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, int n_shared_local, int d_h,
+                        int d_m, int activation, const double* sim, int S, double rho, int flags, const uint16_t* x,
+                        const int32_t* ids_in, const float* weights, int T, int K, int32_t* ids_out,
+                        uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
+                        float* y_partial, void* workspace, size_t workspace_bytes, int32_t* status_dev,
+                        void* stream) {
+  if (expert_lo < 0 || expert_hi > M || expert_hi < expert_lo) return SERE_ERR_DIMENSION;
+  const int m_local = expert_hi - expert_lo;
+  if (m_local + n_shared_local < 1) return SERE_ERR_DIMENSION;
+  int rc = check_layer_shapes(M, n_shared_local, d_h, d_m, activation, T, K);
+  if (rc != SERE_OK) return rc;
+  rc = check_reroute_cfg(K, M, S, rho);
+  if (rc != SERE_OK) return rc;
+  if (sim == nullptr) return SERE_ERR_DIMENSION;
+  if (T == 0) return SERE_OK;
+  return run_layer(bank, M, expert_lo, m_local, n_shared_local, d_h, d_m, activation, sim, S, rho, flags,
+                   MODE_REROUTE | MODE_ALIGN, x, ids_in, weights, T, K, ids_out, expert_class, reroute_map,
+                   active_list, n_active, y_partial, nullptr, workspace, workspace_bytes, status_dev,
+                   static_cast<cudaStream_t>(stream));
+}
+
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router, const float* bias, int T, int d_h, int M, int K,
+                    int32_t* ids, float* weights, float* logits_out, void* stream) {
   if (T < 0 || d_h < 1 || M < 1 || K < 1) return SERE_ERR_DIMENSION;
   if (K > M || K > 32 || M > kMaxExperts) return K > M ? SERE_ERR_CONFIG : SERE_ERR_UNSUPPORTED;
   if (T == 0) return SERE_OK;
   if (!x || !w_router || !ids || !weights) return SERE_ERR_DIMENSION;
   return check_cuda(launch_route_topk(reinterpret_cast<const __nv_bfloat16*>(x),
-                                      reinterpret_cast<const __nv_bfloat16*>(w_router), T, d_h, M, K, ids, weights,
-                                      logits_out, static_cast<cudaStream_t>(stream)));
+                                      reinterpret_cast<const __nv_bfloat16*>(w_router), bias, T, d_h, M, K, ids,
+                                      weights, logits_out, static_cast<cudaStream_t>(stream)));
+}
+
+int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int d_h, float eps, void* stream) {
+  if (T < 0 || d_h < 1) return SERE_ERR_DIMENSION;
+  if (T == 0) return SERE_OK;
+  if (!x || !h_out) return SERE_ERR_DIMENSION;
+  return check_cuda(launch_residual_rmsnorm(x, y, reinterpret_cast<__nv_bfloat16*>(h_out), T, d_h, eps,
+                                            static_cast<cudaStream_t>(stream)));
+}
+
+int sere_set_stage_events(void* const* events, int n) {
+  if (n != 0 && n != kStageEvents) return SERE_ERR_DIMENSION;
+  if (n == 0 || events == nullptr) {
+    t_stage_events_on = false;
+    return SERE_OK;
+  }
+  for (int i = 0; i < kStageEvents; ++i) t_stage_events[i] = static_cast<cudaEvent_t>(events[i]);
+  t_stage_events_on = true;
+  return SERE_OK;
 }
 
 }  // extern "C"

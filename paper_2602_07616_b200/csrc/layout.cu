@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       for (int k = 0; k < K; ++k) {
         const int row = slot_row[t * K + k];
+        if (row < 0) continue;  // expert owned by another rank (expert parallelism)
         const float wk = w[t * K + k];
         const float* src = y_perm + static_cast<size_t>(row) * d_h_pad + f0;
         float4 v = *reinterpret_cast<const float4*>(src);

@@ -30,6 +30,7 @@ struct AlignParams {
   int32_t* row_token;
   int tiles_gu;      // gate/up units per column block
   int units_dn_per;  // down units per column block (tiles_dn * ksplit_dn)
+  int e_lo, m_local; // expert-parallel ownership: bank holds global experts [e_lo, e_lo+m_local)
 };
 
 struct GemmParams {
@@ -47,7 +48,7 @@ struct GemmParams {
 };
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
-size_t reroute_align_smem(int T, int K, int M, int n_shared);
+size_t reroute_align_smem(int T, int K, int M, int Et);
 cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const __nv_bfloat16* wd, int count,
                         const Dims& d, int Et, int first, uint8_t* bank, int unpack, cudaStream_t stream);
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, const int32_t* row_token,
@@ -57,7 +58,10 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            __nv_bfloat16* y_bf16, cudaStream_t stream);
 cudaError_t launch_grouped_gemm(const GemmParams& p, int num_sms, cudaStream_t stream);
 size_t grouped_gemm_smem(int Et);
-cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, int T, int d_h, int M, int K,
-                              int32_t* ids, float* weights, float* logits_out, cudaStream_t stream);
+cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
+                              int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out,
+                              cudaStream_t stream);
+cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
+                                    cudaStream_t stream);
 
 }  // namespace sere

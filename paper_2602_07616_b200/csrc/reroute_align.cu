@@ -28,8 +28,9 @@ namespace sere {
 constexpr int kAlignThreads = 1024;
 constexpr int kAlignWarps = kAlignThreads / 32;
 
-__host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int n_shared) {
-  const int TK = T * K, MW = (M + 31) / 32, Et = M + n_shared;
+// M = global expert count (ids, sim, classes); Et = local groups (bank experts + shared)
+__host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) {
+  const int TK = T * K, MW = (M + 31) / 32;
   size_t b = 0;
   b += static_cast<size_t>(TK) * 4;          // s_ids
   b += static_cast<size_t>(MW) * 4 * 2;      // s_h, s_need
@@ -53,7 +54,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = p.T, K = p.K, M = p.M, S = p.S;
-  const int TK = T * K, MW = (M + 31) / 32, Et = M + p.n_shared;
+  const int TK = T * K, MW = (M + 31) / 32;
+  const int e_lo = p.e_lo, m_loc = p.m_local, Et = m_loc + p.n_shared;  // expert-parallel ownership
   int32_t* s_ids = reinterpret_cast<int32_t*>(smem);
   uint32_t* s_h = reinterpret_cast<uint32_t*>(s_ids + TK);
   uint32_t* s_need = s_h + MW;
@@ -204,8 +206,13 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       return;
     }
   }
-  for (int c = tid; c < TK; c += nthr) atomicAdd(&s_cnt[s_ids[c]], 1);
-  for (int s = tid; s < p.n_shared; s += nthr) s_cnt[M + s] = T;
+  // cells routed to experts this bank does not own (expert parallelism) take no row
+  auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
+  for (int c = tid; c < TK; c += nthr) {
+    const int el = local_of(s_ids[c]);
+    if (el >= 0) atomicAdd(&s_cnt[el], 1);
+  }
+  for (int s = tid; s < p.n_shared; s += nthr) s_cnt[m_loc + s] = T;
   __syncthreads();
 
   const PlanOffsets po = plan_offsets(Et);
@@ -264,9 +271,10 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   uint16_t* wc = s_wc + warp * Et;
   for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
     const int c = c0 + lane;
-    const int e = c < c_hi ? s_ids[c] : -1 - lane;  // unique sentinel for idle lanes
+    const int el = c < c_hi ? local_of(s_ids[c]) : -1;
+    const int e = el >= 0 ? el : -1 - lane;  // unique sentinel for idle / foreign cells
     const unsigned peers = __match_any_sync(0xffffffffu, e);
-    if (c < c_hi && lane == __ffs(peers) - 1) wc[e] += static_cast<uint16_t>(__popc(peers));
+    if (el >= 0 && lane == __ffs(peers) - 1) wc[e] += static_cast<uint16_t>(__popc(peers));
     __syncwarp();
   }
   __syncthreads();
@@ -281,23 +289,26 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   __syncthreads();
   for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
     const int c = c0 + lane;
-    const int e = c < c_hi ? s_ids[c] : -1 - lane;
+    const int el = c < c_hi ? local_of(s_ids[c]) : -1;
+    const int e = el >= 0 ? el : -1 - lane;
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     int base = 0;
-    if (c < c_hi) base = wc[e];
+    if (el >= 0) base = wc[e];
     __syncwarp();
-    if (c < c_hi) {
+    if (el >= 0) {
       const int row = s_row0[e] + base + __popc(peers & ((1u << lane) - 1u));
       p.slot_row[c] = row;
       p.row_token[row] = c / K;
       if (lane == __ffs(peers) - 1) wc[e] = static_cast<uint16_t>(base + __popc(peers));
+    } else if (c < c_hi) {
+      p.slot_row[c] = -1;  // owned by another rank: the combine skips it
     }
     __syncwarp();
   }
   // shared experts: every token, in token order (moe.py:308-309)
   for (int i = tid; i < T * p.n_shared; i += nthr) {
     const int t = i / p.n_shared, s = i % p.n_shared;
-    const int row = s_row0[M + s] + t;
+    const int row = s_row0[m_loc + s] + t;
     p.slot_row[TK + i] = row;
     p.row_token[row] = t;
   }
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 }
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
-  const size_t smem = align_smem_bytes(p.T, p.K, p.M, p.n_shared);
+  const size_t smem = align_smem_bytes(p.T, p.K, p.M, p.m_local + p.n_shared);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(reroute_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -327,6 +338,6 @@ cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-size_t reroute_align_smem(int T, int K, int M, int n_shared) { return align_smem_bytes(T, K, M, n_shared); }
+size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }
 
 }  // namespace sere

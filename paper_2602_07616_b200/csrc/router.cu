@@ -17,7 +17,8 @@ namespace sere {
 constexpr int kTok = 4;
 
 __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* __restrict__ x,
-                                                          const __nv_bfloat16* __restrict__ wr, int T, int d_h,
+                                                          const __nv_bfloat16* __restrict__ wr,
+                                                          const float* __restrict__ bias, int T, int d_h,
                                                           int M, int K, int KS, int32_t* __restrict__ ids,
                                                           float* __restrict__ weights, float* __restrict__ logits_out) {
   extern __shared__ float sm[];
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
   for (int i = threadIdx.x; i < kTok * M; i += blockDim.x) {
     float s = 0.f;
     for (int q = 0; q < KS; ++q) s += s_part[q * kTok * M + i];
+    if (bias) s += bias[i % M];
     s_logit[i] = s;
   }
   __syncthreads();
@@ -89,8 +91,9 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
   }
 }
 
-cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, int T, int d_h, int M, int K,
-                              int32_t* ids, float* weights, float* logits_out, cudaStream_t stream) {
+cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
+                              int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out,
+                              cudaStream_t stream) {
   int KS = 1024 / M;
   if (KS < 1) KS = 1;
   if (KS > 64) KS = 64;
@@ -107,7 +110,39 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
     configured = smem;
   }
   const int blocks = (T + kTok - 1) / kTok;
-  route_topk_kernel<<<blocks, threads, smem, stream>>>(x, w_router, T, d_h, M, K, KS, ids, weights, logits_out);
+  route_topk_kernel<<<blocks, threads, smem, stream>>>(x, w_router, bias, T, d_h, M, K, KS, ids, weights,
+                                                        logits_out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ residual + RMSNorm
+// x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token, fixed-order tree reduction
+__global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
+                                                               __nv_bfloat16* __restrict__ h, int d_h, float eps) {
+  __shared__ float s_red[8];
+  const int t = blockIdx.x;
+  float* xr = x + static_cast<size_t>(t) * d_h;
+  const float* yr = y ? y + static_cast<size_t>(t) * d_h : nullptr;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d_h; i += blockDim.x) {
+    float v = xr[i];
+    if (yr) { v += yr[i]; xr[i] = v; }
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < (blockDim.x + 31) / 32; ++w) tot += s_red[w];
+  const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
+  for (int i = threadIdx.x; i < d_h; i += blockDim.x)
+    h[static_cast<size_t>(t) * d_h + i] = __float2bfloat16_rn(xr[i] * r);
+}
+
+cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
+                                    cudaStream_t stream) {
+  residual_rmsnorm_kernel<<<T, 256, 0, stream>>>(x, y, h_out, d_h, eps);
   return cudaGetLastError();
 }
 

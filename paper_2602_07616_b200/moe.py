@@ -122,20 +122,34 @@ class ExpertBank:
 
     @classmethod
     def random(cls, n_experts: int, n_shared: int, d_h: int, d_m: int, seed: int = 0, device=None,
-               keep_raw: bool = False, chunk: int = 16) -> "ExpertBank":
-        """Seeded N(0, 1/d_h) bf16 weights drawn on the device (moe.py:405-413 distribution),
-        generated and packed `chunk` experts at a time so raw weights never all coexist."""
+               keep_raw: bool = False, chunk: int = 16, expert_ids=None, shared_ids=None) -> "ExpertBank":
+        """Seeded N(0, 1/d_h) bf16 weights drawn on the device (moe.py:405-413 distribution).
+
+        Every expert has its own generator seed derived from (seed, global id), so an
+        expert-parallel shard (`expert_ids` = the global routed ids it owns, `shared_ids`
+        = the shared experts it owns) holds exactly the tensors of the full model.
+        Experts are drawn and packed `chunk` at a time so raw weights never all coexist."""
         torch = _torch()
-        bank = cls(n_experts, n_shared, d_h, d_m, device)
+        expert_ids = list(range(n_experts)) if expert_ids is None else list(expert_ids)
+        shared_ids = list(range(n_shared)) if shared_ids is None else list(shared_ids)
+        bank = cls(len(expert_ids), len(shared_ids), d_h, d_m, device)
+        bank.expert_ids, bank.shared_ids = expert_ids, shared_ids
+        seeds = [int(seed) * 1_000_003 + e for e in expert_ids] + \
+                [int(seed) * 1_000_003 + 10_000_000 + s for s in shared_ids]
         gen = torch.Generator(device=bank.device)
-        gen.manual_seed(int(seed))
         scale = 1.0 / float(np.sqrt(d_h))
         raw = [] if keep_raw else None
-        for first in range(0, bank.n_total, chunk):
-            c = min(chunk, bank.n_total - first)
-            wg = (torch.randn((c, d_h, d_m), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
-            wu = (torch.randn((c, d_h, d_m), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
-            wd = (torch.randn((c, d_m, d_h), generator=gen, device=bank.device) * scale).to(torch.bfloat16)
+        n = len(seeds)
+        for first in range(0, n, chunk):
+            c = min(chunk, n - first)
+            wg = torch.empty((c, d_h, d_m), dtype=torch.bfloat16, device=bank.device)
+            wu = torch.empty_like(wg)
+            wd = torch.empty((c, d_m, d_h), dtype=torch.bfloat16, device=bank.device)
+            for j in range(c):
+                gen.manual_seed(seeds[first + j])
+                wg[j] = torch.randn((d_h, d_m), generator=gen, device=bank.device) * scale
+                wu[j] = torch.randn((d_h, d_m), generator=gen, device=bank.device) * scale
+                wd[j] = torch.randn((d_m, d_h), generator=gen, device=bank.device) * scale
             bank.pack(wg, wu, wd, first)
             if raw is not None:
                 raw.append((wg, wu, wd))
@@ -246,8 +260,53 @@ def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: floa
     return out
 
 
-def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False):
-    """moe.py:268-277 on CUDA: w_router bf16 [d_h,M], x bf16 [T,d_h] -> (ids int32, weights f32[, logits])."""
+def moe_forward_ep_device(bank: ExpertBank, n_experts: int, expert_lo: int, sim, retain_count: int,
+                          threshold: float, x, ids, weights, activation: str = "silu", stream=None,
+                          out: LayerOutput | None = None) -> LayerOutput:
+    """Expert-parallel shard of `moe_forward_device` (`sere_moe_forward_ep`): re-route the
+    full gathered [T,K] table against `sim` (global ids, M = n_experts), then evaluate only
+    this bank's experts (global [expert_lo, expert_lo + bank.M) + its shared experts).
+    out.y = this rank's partial layer output; the ranks' partials sum to moe.layer_forward."""
+    torch = _torch()
+    cfg = _rr.RerouteConfig(retain_count, threshold)
+    x = x.to(torch.bfloat16).contiguous()
+    ids = ids.to(torch.int32).contiguous()
+    weights = weights.to(torch.float32).contiguous()
+    T, K = int(ids.shape[0]), int(ids.shape[1])
+    if x.shape != (T, bank.d_h) or weights.shape != ids.shape:
+        raise DimensionError("x / ids / weights shapes disagree")
+    if cfg.retain_count > K:
+        raise ConfigError(f"retain_count must not exceed K (got S={cfg.retain_count}, K={K})")
+    dsim = _rr.as_device_sim(sim, bank.device)
+    if dsim.m != n_experts:
+        raise DimensionError(f"similarity matrix is {dsim.m}x{dsim.m}, expected {n_experts}")
+    dev = bank.device
+    if out is None:
+        rr = _rr.DeviceReroute(
+            new_indices=torch.empty((T, K), dtype=torch.int32, device=dev),
+            expert_class=torch.empty(n_experts, dtype=torch.uint8, device=dev),
+            reroute_map=torch.empty(n_experts, dtype=torch.int32, device=dev),
+            active_list=torch.empty(n_experts, dtype=torch.int32, device=dev),
+            n_active=torch.empty(1, dtype=torch.int32, device=dev),
+            status=torch.zeros(1, dtype=torch.int32, device=dev),
+        )
+        out = LayerOutput(torch.empty((T, bank.d_h), dtype=torch.float32, device=dev), None, rr.status, rr)
+    rr = out.reroute
+    flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    _lib.call("sere_moe_forward_ep", bank.data.data_ptr(), int(n_experts), int(expert_lo),
+              int(expert_lo) + bank.M, bank.n_shared, bank.d_h, bank.d_m, activation_code(activation),
+              dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags, x.data_ptr(), ids.data_ptr(),
+              weights.data_ptr(), T, K, rr.new_indices.data_ptr(), rr.expert_class.data_ptr(),
+              rr.reroute_map.data_ptr(), rr.active_list.data_ptr(), rr.n_active.data_ptr(), out.y.data_ptr(),
+              ws.data_ptr(), ws.numel(), out.status.data_ptr(), _stream_ptr(stream))
+    dsim.validated = True
+    return out
+
+
+def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False, bias=None, out=None):
+    """moe.py:268-277 on CUDA: w_router bf16 [d_h,M], x bf16 [T,d_h] -> (ids int32, weights f32[, logits]).
+    `bias` (f32 [M], optional) is the benchmark's popularity-skew knob added to the logits."""
     torch = _torch()
     x = x.to(torch.bfloat16).contiguous()
     w = w_router.to(torch.bfloat16).contiguous()
@@ -257,10 +316,15 @@ def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False
     M = int(w.shape[1])
     if not 1 <= top_k <= M:
         raise ConfigError(f"top_k must satisfy 1 <= K <= M (got K={top_k}, M={M})")
-    ids = torch.empty((T, top_k), dtype=torch.int32, device=x.device)
-    wts = torch.empty((T, top_k), dtype=torch.float32, device=x.device)
+    if out is not None:
+        ids, wts = out
+    else:
+        ids = torch.empty((T, top_k), dtype=torch.int32, device=x.device)
+        wts = torch.empty((T, top_k), dtype=torch.float32, device=x.device)
     lg = torch.empty((T, M), dtype=torch.float32, device=x.device) if logits else None
-    _lib.call("sere_route_topk", x.data_ptr(), w.data_ptr(), T, d_h, M, int(top_k), ids.data_ptr(),
+    b = bias.to(torch.float32).contiguous() if bias is not None else None
+    _lib.call("sere_route_topk", x.data_ptr(), w.data_ptr(), b.data_ptr() if b is not None else None,
+              T, d_h, M, int(top_k), ids.data_ptr(),
               wts.data_ptr(), lg.data_ptr() if lg is not None else None, _stream_ptr(stream))
     return (ids, wts, lg) if logits else (ids, wts)
 
