@@ -39,7 +39,15 @@ thread_local cudaEvent_t t_stage_events[kStageEvents];
 thread_local bool t_stage_events_on = false;
 
 inline void stage_mark(int i, cudaStream_t stream) {
-  if (t_stage_events_on) cudaEventRecord(t_stage_events[i], stream);
+  if (!t_stage_events_on) return;
+  // under stream capture a plain record only marks a dependency; an external record
+  // becomes a real event-record node of the graph, so the timestamps exist after replay
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(t_stage_events[i], stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(t_stage_events[i], stream);
 }
 
 struct WsLayout {
