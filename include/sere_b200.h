@@ -136,6 +136,19 @@ int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, in
                      size_t workspace_bytes, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------
+ * (4a) Decode block = (4) with the residual add and the next layer's RMSNorm fused
+ *     into the combine pass: x_residual += MoE(h);  h_next = bf16(x_residual *
+ *     rsqrt(mean(x_residual^2) + eps)).  y (f32 [T,d_h]) is optional (NULL skips it).
+ *     The Qwen3-style pre-norm block of the 48-layer benchmark step.
+ * ------------------------------------------------------------------------ */
+int sere_moe_block_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation,
+                           const double* sim, int S, double rho, int flags, const uint16_t* h,
+                           const int32_t* ids_in, const float* weights, int T, int K, int32_t* ids_out,
+                           uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
+                           int32_t* n_active, float* x_residual, uint16_t* h_next, float eps, float* y,
+                           void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
  * (4b) Expert-parallel shard of (4): the bank holds only global experts
  *     [expert_lo, expert_hi) (as bank slots 0..) plus n_shared_local shared
  *     experts. Re-routing runs on the FULL gathered [T,K] table (every rank
@@ -155,12 +168,19 @@ int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, i
 /* ------------------------------------------------------------------------
  * (5) Router: logits = x W_r (fp32 accumulate), top-K with ties to the lower
  *     index, softmax over the K picks.  Replaces moe.route_topk / topk_softmax
- *     (moe.py:248-277).  w_router bf16 [d_h, M] (reference orientation).
+ *     (moe.py:248-277).
+ *  w_router_t bf16 [M, d_h]: RouterWeights.w_router TRANSPOSED (expert-major, K
+ *     contiguous -- converted once at load, the router is static).
+ *  bias f32 [M] (nullable) is added to the logits before selection: the benchmark's
+ *     expert-popularity skew knob; NULL reproduces moe.route_topk.
+ *  logits_out f32 [T,M] (nullable).  workspace: >= sere_route_workspace_bytes(T,d_h,M)
+ *     bytes, ZERO-FILLED before its first use (it holds per-tile tickets that every
+ *     launch leaves at zero again).
  * ------------------------------------------------------------------------ */
-int sere_route_topk(const uint16_t* x, const uint16_t* w_router, const float* bias, int T, int d_h, int M,
-                    int K, int32_t* ids, float* weights, float* logits_out, void* stream);
-/*   bias f32 [M] (nullable) is added to the logits before selection: the benchmark's
- *   expert-popularity skew knob; NULL reproduces moe.route_topk.      */
+size_t sere_route_workspace_bytes(int T, int d_h, int M);
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router_t, const float* bias, int T, int d_h, int M,
+                    int K, int32_t* ids, float* weights, float* logits_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * (6) Decode-block glue: x += y (fp32 residual stream, y nullable) and

@@ -58,10 +58,14 @@ SIGNATURES = {
                                     _p, _p, _p, _c_size, _p, _p]),
     "sere_moe_forward": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _c_double, _c_int,
                                   _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p, _p, _c_size, _p, _p]),
+    "sere_moe_block_forward": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int, _c_double,
+                                        _c_int, _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p,
+                                        ctypes.c_float, _p, _p, _c_size, _p, _p]),
     "sere_moe_forward_ep": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int,
                                      _c_double, _c_int, _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p,
                                      _c_size, _p, _p]),
-    "sere_route_topk": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p]),
+    "sere_route_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
+    "sere_route_topk": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _c_size, _p]),
     "sere_residual_rmsnorm": (_c_int, [_p, _p, _p, _c_int, _c_int, ctypes.c_float, _p]),
     "sere_set_stage_events": (_c_int, [ctypes.POINTER(ctypes.c_void_p), _c_int]),
     "sere_layer_workspace_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int,

@@ -106,11 +106,13 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
               double rho, int flags, int mode, const uint16_t* x, const int32_t* ids_in, const float* weights,
               int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
               int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
-              int32_t* status_dev, cudaStream_t stream) {
+              int32_t* status_dev, cudaStream_t stream, float* x_res = nullptr, uint16_t* h_next = nullptr,
+              float eps = 0.f) {
   const WsLayout L = ws_layout(T, K, m_local, n_shared, d_h, d_m);
   if (workspace == nullptr || workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
-  if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr || y == nullptr)
+  if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr)
     return SERE_ERR_DIMENSION;
+  if (y == nullptr && (x_res == nullptr || h_next == nullptr)) return SERE_ERR_DIMENSION;
   uint8_t* ws = reinterpret_cast<uint8_t*>(align_up(reinterpret_cast<uintptr_t>(workspace), 1024));
   int32_t* plan = reinterpret_cast<int32_t*>(ws + L.plan);
   int32_t* slot_row = reinterpret_cast<int32_t*>(ws + L.slot_row);
@@ -183,7 +185,8 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 
   stage_mark(4, stream);
   e = launch_combine(y_perm, d, L.r_max, plan, slot_row, weights, T, K, n_shared, y,
-                     reinterpret_cast<__nv_bfloat16*>(y_bf16), stream);
+                     reinterpret_cast<__nv_bfloat16*>(y_bf16), x_res, reinterpret_cast<__nv_bfloat16*>(h_next), eps,
+                     stream);
   stage_mark(5, stream);
   return check_cuda(e);
 }
@@ -332,6 +335,24 @@ int sere_moe_forward(const void* bank, int M, int n_shared, int d_h, int d_m, in
                    workspace, workspace_bytes, status_dev, static_cast<cudaStream_t>(stream));
 }
 
+int sere_moe_block_forward(const void* bank, int M, int n_shared, int d_h, int d_m, int activation,
+                           const double* sim, int S, double rho, int flags, const uint16_t* h,
+                           const int32_t* ids_in, const float* weights, int T, int K, int32_t* ids_out,
+                           uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
+                           float* x_residual, uint16_t* h_next, float eps, float* y, void* workspace,
+                           size_t workspace_bytes, int32_t* status_dev, void* stream) {
+  int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
+  if (rc != SERE_OK) return rc;
+  rc = check_reroute_cfg(K, M, S, rho);
+  if (rc != SERE_OK) return rc;
+  if (sim == nullptr || x_residual == nullptr || h_next == nullptr) return SERE_ERR_DIMENSION;
+  if (T == 0) return SERE_OK;
+  return run_layer(bank, M, 0, M, n_shared, d_h, d_m, activation, sim, S, rho, flags, MODE_REROUTE | MODE_ALIGN, h,
+                   ids_in, weights, T, K, ids_out, expert_class, reroute_map, active_list, n_active, y, nullptr,
+                   workspace, workspace_bytes, status_dev, static_cast<cudaStream_t>(stream), x_residual, h_next,
+                   eps);
+}
+
 int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, int n_shared_local, int d_h,
                         int d_m, int activation, const double* sim, int S, double rho, int flags, const uint16_t* x,
                         const int32_t* ids_in, const float* weights, int T, int K, int32_t* ids_out,
@@ -353,12 +374,24 @@ int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, i
                    static_cast<cudaStream_t>(stream));
 }
 
-int sere_route_topk(const uint16_t* x, const uint16_t* w_router, const float* bias, int T, int d_h, int M, int K,
-                    int32_t* ids, float* weights, float* logits_out, void* stream) {
+size_t sere_route_workspace_bytes(int T, int d_h, int M) {
+  if (T < 0 || d_h < 1 || M < 1) return 0;
+  return route_workspace_bytes(T, d_h, M);
+}
+
+int sere_route_topk(const uint16_t* x, const uint16_t* w_router_t, const float* bias, int T, int d_h, int M, int K,
+                    int32_t* ids, float* weights, float* logits_out, void* workspace, size_t workspace_bytes,
+                    void* stream) {
   if (T < 0 || d_h < 1 || M < 1 || K < 1) return SERE_ERR_DIMENSION;
   if (K > M || K > 32 || M > kMaxExperts) return K > M ? SERE_ERR_CONFIG : SERE_ERR_UNSUPPORTED;
   if (T == 0) return SERE_OK;
-  if (!x || !w_router || !ids || !weights) return SERE_ERR_DIMENSION;
+  if (!x || !w_router_t || !ids || !weights) return SERE_ERR_DIMENSION;
+  const __nv_bfloat16* w_router = reinterpret_cast<const __nv_bfloat16*>(w_router_t);
+  if (route_fast_path(M, K, d_h)) {
+    if (workspace == nullptr || workspace_bytes < route_workspace_bytes(T, d_h, M)) return SERE_ERR_WORKSPACE;
+    return check_cuda(launch_route_mma(reinterpret_cast<const __nv_bfloat16*>(x), w_router, bias, T, d_h, M, K, ids,
+                                       weights, logits_out, workspace, static_cast<cudaStream_t>(stream)));
+  }
   return check_cuda(launch_route_topk(reinterpret_cast<const __nv_bfloat16*>(x),
                                       reinterpret_cast<const __nv_bfloat16*>(w_router), bias, T, d_h, M, K, ids,
                                       weights, logits_out, static_cast<cudaStream_t>(stream)));

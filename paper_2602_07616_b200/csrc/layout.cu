@@ -179,27 +179,39 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 // y[t] = sum_k w[t,k] * Y[slot_row[t,k]]  (k ascending)  + sum_s Y[shared row]   (moe.py:302-309)
 // Y = sum over down-GEMM K splits in split order. Products and sums rounded
 // separately (no FMA contraction), mirroring numpy's `y[rows] += w * E(x)`.
+// Optional decode-block epilogue (x_res != null): x_res[t] += y[t], then
+// h_next[t] = bf16(x_res[t] * rsqrt(mean(x_res[t]^2) + eps)) -- the residual add and the
+// next layer's RMSNorm fused into the same pass over the token row (one CTA per token).
+__device__ __forceinline__ float4 load_y_sum(const float* src, int ksplit, size_t split_stride) {
+  float4 v = *reinterpret_cast<const float4*>(src);
+  for (int s = 1; s < ksplit; ++s) {
+    const float4 o = *reinterpret_cast<const float4*>(src + s * split_stride);
+    v.x = __fadd_rn(v.x, o.x); v.y = __fadd_rn(v.y, o.y); v.z = __fadd_rn(v.z, o.z); v.w = __fadd_rn(v.w, o.w);
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
                                                       int d_h, int d_h_pad, const int32_t* __restrict__ plan,
                                                       const int32_t* __restrict__ slot_row,
                                                       const float* __restrict__ w, int T, int K, int n_shared,
-                                                      float* __restrict__ y, __nv_bfloat16* __restrict__ y_bf16) {
+                                                      float* __restrict__ y, __nv_bfloat16* __restrict__ y_bf16,
+                                                      float* __restrict__ x_res, __nv_bfloat16* __restrict__ h_next,
+                                                      float eps) {
+  __shared__ float s_red[8];
   if (plan[P_STATUS] != 0) return;
   const int TK = T * K;
   const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
+  const bool vec = (d_h & 3) == 0;
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    float ss = 0.f;
     for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       for (int k = 0; k < K; ++k) {
         const int row = slot_row[t * K + k];
         if (row < 0) continue;  // expert owned by another rank (expert parallelism)
         const float wk = w[t * K + k];
-        const float* src = y_perm + static_cast<size_t>(row) * d_h_pad + f0;
-        float4 v = *reinterpret_cast<const float4*>(src);
-        for (int s = 1; s < ksplit; ++s) {
-          const float4 o = *reinterpret_cast<const float4*>(src + s * split_stride);
-          v.x = __fadd_rn(v.x, o.x); v.y = __fadd_rn(v.y, o.y); v.z = __fadd_rn(v.z, o.z); v.w = __fadd_rn(v.w, o.w);
-        }
+        const float4 v = load_y_sum(y_perm + static_cast<size_t>(row) * d_h_pad + f0, ksplit, split_stride);
         acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, v.x));
         acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, v.y));
         acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, v.z));
@@ -207,39 +219,53 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
       }
       for (int s = 0; s < n_shared; ++s) {
         const int row = slot_row[TK + t * n_shared + s];
-        const float* src = y_perm + static_cast<size_t>(row) * d_h_pad + f0;
-        float4 v = *reinterpret_cast<const float4*>(src);
-        for (int q = 1; q < ksplit; ++q) {
-          const float4 o = *reinterpret_cast<const float4*>(src + q * split_stride);
-          v.x = __fadd_rn(v.x, o.x); v.y = __fadd_rn(v.y, o.y); v.z = __fadd_rn(v.z, o.z); v.w = __fadd_rn(v.w, o.w);
-        }
+        const float4 v = load_y_sum(y_perm + static_cast<size_t>(row) * d_h_pad + f0, ksplit, split_stride);
         acc[0] = __fadd_rn(acc[0], v.x);
         acc[1] = __fadd_rn(acc[1], v.y);
         acc[2] = __fadd_rn(acc[2], v.z);
         acc[3] = __fadd_rn(acc[3], v.w);
       }
-      float* dst = y + static_cast<size_t>(t) * d_h + f0;
-      if ((d_h & 3) == 0) {
-        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      } else {
-        for (int q = 0; q < 4 && f0 + q < d_h; ++q) dst[q] = acc[q];
+      const size_t o = static_cast<size_t>(t) * d_h + f0;
+      if (y) {
+        if (vec) *reinterpret_cast<float4*>(y + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        else for (int q = 0; q < 4 && f0 + q < d_h; ++q) y[o + q] = acc[q];
       }
-      if (y_bf16) {
-        __nv_bfloat16* db = y_bf16 + static_cast<size_t>(t) * d_h + f0;
-        for (int q = 0; q < 4 && f0 + q < d_h; ++q) db[q] = __float2bfloat16_rn(acc[q]);
+      if (y_bf16)
+        for (int q = 0; q < 4 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[q]);
+      if (x_res) {
+        for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+          const float v = x_res[o + q] + acc[q];
+          x_res[o + q] = v;
+          ss = fmaf(v, v, ss);
+        }
       }
+    }
+    if (x_res) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
+      __syncthreads();
+      float tot = 0.f;
+      for (int i = 0; i < (blockDim.x + 31) / 32; ++i) tot += s_red[i];
+      const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
+      for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
+        const size_t o = static_cast<size_t>(t) * d_h + f0;
+        for (int q = 0; q < 4 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(x_res[o + q] * r);
+      }
+      __syncthreads();
     }
   }
 }
 
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
-                           __nv_bfloat16* y_bf16, cudaStream_t stream) {
+                           __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
+                           cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   int threads = d.d_h / 4 >= 256 ? 256 : ((d.d_h / 4 + 31) / 32) * 32;
   if (threads < 32) threads = 32;
   combine_kernel<<<T, threads, 0, stream>>>(y_perm, d.ksplit_dn, r_max, d.d_h, d.d_h_pad, plan, slot_row, w, T, K,
-                                            n_shared, y, y_bf16);
+                                            n_shared, y, y_bf16, x_res, h_next, eps);
   return cudaGetLastError();
 }
 

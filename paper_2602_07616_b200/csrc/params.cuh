@@ -55,12 +55,18 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
                            int r_max, uint8_t* x_pack, int num_sms, cudaStream_t stream);
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
-                           __nv_bfloat16* y_bf16, cudaStream_t stream);
+                           __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
+                           cudaStream_t stream);
 cudaError_t launch_grouped_gemm(const GemmParams& p, int num_sms, cudaStream_t stream);
 size_t grouped_gemm_smem(int Et);
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
                               int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out,
                               cudaStream_t stream);
+cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
+                             int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out, void* ws,
+                             cudaStream_t stream);
+size_t route_workspace_bytes(int T, int d_h, int M);
+bool route_fast_path(int M, int K, int d_h);
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
                                     cudaStream_t stream);
 

@@ -34,7 +34,7 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   size_t b = 0;
   b += static_cast<size_t>(TK) * 4;          // s_ids
   b += static_cast<size_t>(MW) * 4 * 2;      // s_h, s_need
-  b += static_cast<size_t>(M) * 4;           // s_map
+  b += static_cast<size_t>(M) * 4 * 2;       // s_map, s_list
   b += static_cast<size_t>(Et) * 4 * 3;      // s_cnt, s_row0, s_gidx
   b += static_cast<size_t>(round_up(M, 4));  // s_cls
   b += static_cast<size_t>(kAlignWarps) * Et * 2;  // s_wc
@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   uint32_t* s_h = reinterpret_cast<uint32_t*>(s_ids + TK);
   uint32_t* s_need = s_h + MW;
   int32_t* s_map = reinterpret_cast<int32_t*>(s_need + MW);
-  int32_t* s_cnt = s_map + M;
+  int32_t* s_list = s_map + M;  // compact list of needed secondaries
+  int32_t* s_cnt = s_list + M;
   int32_t* s_row0 = s_cnt + Et;
   int32_t* s_gidx = s_row0 + Et;
   uint8_t* s_cls = reinterpret_cast<uint8_t*>(s_gidx + Et);
@@ -120,26 +121,55 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       }
     }
     __syncthreads();
-    // ---- per-secondary argmax over the primary set, one warp per expert (rerouting.py:78-97,157-164)
-    for (int e = warp; e < M; e += nwarps) {
-      if (!((s_need[e >> 5] >> (e & 31)) & 1u)) continue;
+    // ---- compact list of the needed secondaries (ascending)
+    __shared__ int s_nneed;
+    if (warp == 0) {
+      int base = 0;
+      for (int c0 = 0; c0 < M; c0 += 32) {
+        const int e = c0 + lane;
+        const bool nd = e < M && ((s_need[e >> 5] >> (e & 31)) & 1u);
+        const unsigned m = __ballot_sync(0xffffffffu, nd);
+        if (nd) s_list[base + __popc(m & ((1u << lane) - 1u))] = e;
+        base += __popc(m);
+      }
+      if (lane == 0) s_nneed = base;
+    }
+    __syncthreads();
+    // ---- per-secondary argmax over the primary set (rerouting.py:78-97,157-164): one 16-lane
+    // group per secondary u; every lane first issues all its loads of row u (independent, so
+    // they overlap), then compares ascending with strict '>' and the group reduces to the
+    // first maximum (larger value, then lower index).
+    const int n_need = s_nneed;
+    const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
+    for (int base = 0; base < n_need; base += ngrp) {
+      const int li = base + grp;
+      const bool have = li < n_need;
+      const int e = have ? s_list[li] : 0;
       const double* row = p.sim + static_cast<size_t>(e) * M;
       double bs = -CUDART_INF;
       int bi = -1;
-      for (int v = lane; v < M; v += 32) {  // ascending per lane, strict '>'
-        if ((s_h[v >> 5] >> (v & 31)) & 1u) {
-          const double s = row[v];
-          if (s > bs) { bs = s; bi = v; }
+      if (have) {
+        for (int v0 = 0; v0 < M; v0 += 16 * 8) {
+          double vals[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int v = v0 + glane + 16 * j;
+            vals[j] = v < M ? __ldg(row + v) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int v = v0 + glane + 16 * j;
+            if (v < M && ((s_h[v >> 5] >> (v & 31)) & 1u) && vals[j] > bs) { bs = vals[j]; bi = v; }
+          }
         }
       }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        // the global first maximum of an ascending strict-'>' scan: larger value, then lower index
+      for (int off = 8; off > 0; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, off, 16);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off, 16);
         if (oi >= 0 && (bi < 0 || os > bs || (os == bs && oi < bi))) { bs = os; bi = oi; }
       }
-      if (lane == 0) {
+      if (have && glane == 0) {
         if (p.rho > 0.0 && bs < p.rho) {
           s_cls[e] = SERE_CLASS_CRITICAL;  // preserved (rerouting.py:160-161)
         } else {

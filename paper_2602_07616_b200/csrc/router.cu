@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
 #pragma unroll
     for (int j = 0; j < kTok; ++j) acc[j] = 0.f;
     for (int k = k0; k < k1; ++k) {
-      const float w = __bfloat162float(wr[static_cast<size_t>(k) * M + e]);
+      const float w = __bfloat162float(wr[static_cast<size_t>(e) * d_h + k]);  // W_r^T [M, d_h]
 #pragma unroll
       for (int j = 0; j < kTok; ++j) acc[j] = fmaf(__bfloat162float(s_x[j * d_h + k]), w, acc[j]);
     }
@@ -89,6 +89,169 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
       for (int r = 0; r < K; ++r) weights[static_cast<size_t>(t) * K + r] = sel_val[r] / den;
     }
   }
+}
+
+// ------------------------------------------------------------------ fast path
+// Tensor-core router for M <= 256, M % 8 == 0, K <= 32: grid (T/32 token tiles, d_h/256
+// K-splits); each CTA stages a 32 x 256 slice of x and the transposed 256 x M slice of
+// W_r in shared memory and issues bf16 mma.sync m16n8k16 (fp32 accumulate): the router
+// GEMM is 0.27 GFLOP/layer and purely latency-bound, so it needs many small CTAs, not
+// TMEM. Partial logits go to the workspace; the LAST CTA of each token tile (atomic
+// ticket) sums the splits in split order (deterministic), adds the bias and runs the
+// warp top-K + softmax, then resets its ticket for the next launch.
+constexpr int kRtTok = 32, kRtKC = 256, kRtPad = 8;
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256) route_mma_kernel(const __nv_bfloat16* __restrict__ x,
+                                                        const __nv_bfloat16* __restrict__ wr,
+                                                        const float* __restrict__ bias, int T, int d_h, int M, int K,
+                                                        int nsplit, float* __restrict__ part,
+                                                        int32_t* __restrict__ tickets, int32_t* __restrict__ ids,
+                                                        float* __restrict__ weights, float* __restrict__ logits_out) {
+  extern __shared__ __align__(16) uint8_t rsm[];
+  constexpr int LD = kRtKC + kRtPad;  // padded row (bank-conflict-free fragment loads)
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(rsm);        // [32][LD]
+  __nv_bfloat16* wt = xs + kRtTok * LD;                             // [M][LD]  (W_r transposed)
+  __shared__ int s_last;
+  const int t0 = blockIdx.x * kRtTok, split = blockIdx.y, k0 = split * kRtKC;
+  const int kn = min(kRtKC, d_h - k0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int CPR = kRtKC / 8;  // 16-B chunks per staged row (d_h % 8 == 0 on this path)
+  for (int i = tid; i < kRtTok * CPR; i += blockDim.x) {
+    const int t = i / CPR, k = (i % CPR) * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (t0 + t < T && k < kn) v = *reinterpret_cast<const uint4*>(x + static_cast<size_t>(t0 + t) * d_h + k0 + k);
+    *reinterpret_cast<uint4*>(xs + t * LD + k) = v;
+  }
+  for (int i = tid; i < M * CPR; i += blockDim.x) {  // W_r^T rows: expert-major, K contiguous
+    const int e = i / CPR, k = (i % CPR) * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (k < kn) v = *reinterpret_cast<const uint4*>(wr + static_cast<size_t>(e) * d_h + k0 + k);
+    *reinterpret_cast<uint4*>(wt + e * LD + k) = v;
+  }
+  __syncthreads();
+  const int g = lane >> 2, tg = lane & 3;
+  const int th = warp & 1;                 // token half: rows 16*th .. +16
+  const int n_tiles = M / 8;
+  float acc[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  const __nv_bfloat16* xa = xs + (16 * th + g) * LD + tg * 2;
+  for (int kk = 0; kk < kRtKC; kk += 16) {
+    const uint32_t a0 = *reinterpret_cast<const uint32_t*>(xa + kk);
+    const uint32_t a1 = *reinterpret_cast<const uint32_t*>(xa + 8 * LD + kk);
+    const uint32_t a2 = *reinterpret_cast<const uint32_t*>(xa + kk + 8);
+    const uint32_t a3 = *reinterpret_cast<const uint32_t*>(xa + 8 * LD + kk + 8);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int nt = (warp >> 1) + 4 * j;
+      if (nt < n_tiles) {
+        const __nv_bfloat16* wb = wt + (nt * 8 + g) * LD + tg * 2 + kk;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wb);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wb + 8);
+        mma_bf16_16816(acc[j], a0, a1, a2, a3, b0, b1);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int nt = (warp >> 1) + 4 * j;
+    if (nt < n_tiles) {
+      const int e = nt * 8 + tg * 2;
+      const int ta = t0 + 16 * th + g, tb = ta + 8;
+      float* pp = part + static_cast<size_t>(split) * T * M;
+      if (ta < T) { pp[static_cast<size_t>(ta) * M + e] = acc[j][0]; pp[static_cast<size_t>(ta) * M + e + 1] = acc[j][1]; }
+      if (tb < T) { pp[static_cast<size_t>(tb) * M + e] = acc[j][2]; pp[static_cast<size_t>(tb) * M + e + 1] = acc[j][3]; }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(&tickets[blockIdx.x], 1) == nsplit - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int tl = warp; tl < kRtTok; tl += blockDim.x / 32) {
+    const int t = t0 + tl;
+    if (t >= T) break;
+    float lg[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int v = lane + 32 * j;
+      float s = -CUDART_INF_F;
+      if (v < M) {
+        s = 0.f;
+        for (int q = 0; q < nsplit; ++q) s += __ldcg(part + (static_cast<size_t>(q) * T + t) * M + v);
+        if (bias) s += bias[v];
+        if (logits_out) logits_out[static_cast<size_t>(t) * M + v] = s;
+      }
+      lg[j] = s;
+    }
+    float top = 0.f, den = 0.f, my_w = 0.f;
+    int my_id = 0;
+    for (int r = 0; r < K; ++r) {
+      float bv = -CUDART_INF_F;
+      int bi = -1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int v = lane + 32 * j;
+        if (v < M && (bi < 0 || lg[j] > bv)) { bv = lg[j]; bi = v; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+      }
+      if (r == 0) top = bv;
+      const float ex = expf(bv - top);
+      den += ex;
+      if (lane == r) { my_id = bi; my_w = ex; }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (lane + 32 * j == bi) lg[j] = -CUDART_INF_F;
+    }
+    if (lane < K) {
+      ids[static_cast<size_t>(t) * K + lane] = my_id;
+      weights[static_cast<size_t>(t) * K + lane] = my_w / den;
+    }
+  }
+  if (tid == 0) tickets[blockIdx.x] = 0;
+}
+
+size_t route_workspace_bytes(int T, int d_h, int M) {
+  const int nsplit = (d_h + kRtKC - 1) / kRtKC;
+  const int tiles = (T + kRtTok - 1) / kRtTok;
+  return 256 + static_cast<size_t>(tiles) * 4 + static_cast<size_t>(nsplit) * T * M * 4;
+}
+
+bool route_fast_path(int M, int K, int d_h) { return M % 8 == 0 && M <= 256 && K <= 32 && d_h % 8 == 0; }
+
+cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
+                             int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out, void* ws,
+                             cudaStream_t stream) {
+  const int nsplit = (d_h + kRtKC - 1) / kRtKC;
+  const int tiles = (T + kRtTok - 1) / kRtTok;
+  int32_t* tickets = reinterpret_cast<int32_t*>(ws);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((tiles * 4 + 255) / 256) * 256);
+  const size_t smem = static_cast<size_t>(kRtTok + M) * (kRtKC + kRtPad) * 2;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(route_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  route_mma_kernel<<<dim3(tiles, nsplit), 256, smem, stream>>>(x, w_router, bias, T, d_h, M, K, nsplit, part,
+                                                               tickets, ids, weights, logits_out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,

@@ -60,9 +60,10 @@ def uniform_sim(rng: np.random.Generator, m: int) -> np.ndarray:
 @dataclass
 class DecodeLayer:
     bank: Any            # moe.ExpertBank
-    w_router: Any        # bf16 [d_h, M]
+    w_router: Any        # bf16 [d_h, M] (reference orientation)
     bias: Any            # f32 [M] popularity skew (beta * N(0,1)); zeros for beta = 0
     sim: Any             # rerouting.DeviceSimilarity (fp64 [M,M])
+    w_router_t: Any = None  # bf16 [M, d_h] kernel orientation
 
 
 class DecodeModel:
@@ -92,7 +93,8 @@ class DecodeModel:
             rng = np.random.default_rng([seed, l, 3])
             sim = clustered_sim(rng, M) if sim_kind == "clustered" else uniform_sim(rng, M)
             self.sims_host.append(sim)
-            self.layers.append(DecodeLayer(bank, wr, bias, _rr.DeviceSimilarity(sim, self.device)))
+            self.layers.append(DecodeLayer(bank, wr, bias, _rr.DeviceSimilarity(sim, self.device),
+                                           _moe.router_weight_t(wr)))
 
     @property
     def weight_bytes_per_expert(self) -> int:
@@ -163,8 +165,8 @@ class DecodeStep(StageEvents):
                 n_active=torch.zeros(1, dtype=torch.int32, device=dev),
                 status=torch.zeros(1, dtype=torch.int32, device=dev),
             )
-            self.outs.append(_moe.LayerOutput(torch.zeros((T, model.d_h), dtype=torch.float32, device=dev), None,
-                                              rr.status, rr))
+            y = torch.zeros((T, model.d_h), dtype=torch.float32, device=dev) if block == "plain" else None
+            self.outs.append(_moe.LayerOutput(y, None, rr.status, rr))
         self.graph = None
         self.stage_events = None
         _moe.workspace(T, model.K, model.M, model.n_shared, model.d_h, model.d_m, dev)
@@ -187,21 +189,22 @@ class DecodeStep(StageEvents):
                     self.h.copy_(self.x)
                 else:
                     self.h.copy_(self.outs[l - 1].y)
-            _moe.route_topk_device(layer.w_router, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
+            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
             self._events_on(l)
-            _moe.moe_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
-                                    out=self.outs[l])
+            if plain:
+                _moe.moe_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
+                                        out=self.outs[l])
+            else:  # x += MoE(h); h = RMSNorm(x) fused into the combine pass
+                _moe.moe_block_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
+                                              self.x, self.h, self.eps, out=self.outs[l])
             self._events_off()
-            if not plain:
-                self._norm(self.outs[l].y)
         if plain:
             self.x.copy_(self.outs[-1].y)
 
     @property
     def launches_per_step(self) -> int:
-        """Kernels of this library per step: router + 5 layer kernels (+ RMSNorm) per layer."""
-        per_layer = 6 + (0 if self.block == "plain" else 1)
-        return self.model.L * per_layer + (0 if self.block == "plain" else 1)
+        """Kernels of this library per step: router + 5 layer kernels per layer (+ the first RMSNorm)."""
+        return self.model.L * 6 + (0 if self.block == "plain" else 1)
 
     def run(self) -> None:
         """One step on the current stream (graph replay if captured)."""

@@ -176,7 +176,7 @@ class EPDecodeStep(StageEvents):
         self.x.copy_(self.x_in)
         self._norm(None)
         for l, layer in enumerate(m.layers):
-            _moe.route_topk_device(layer.w_router, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
+            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
             h_all, ids_all, w_all = self.xch.gather(self.h, self.ids, self.w)
             self._events_on(l)
             _moe.moe_forward_ep_device(layer.bank, m.M, self.lo, layer.sim, self.S, self.rho, h_all, ids_all,

@@ -260,6 +260,43 @@ def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: floa
     return out
 
 
+def moe_block_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: float, h, ids, weights,
+                             x_residual, h_next, eps: float = 1e-6, activation: str = "silu", stream=None,
+                             out: LayerOutput | None = None, want_y: bool = False) -> LayerOutput:
+    """Decode block (`sere_moe_block_forward`): x_residual += SERE-MoE(h) and
+    h_next = bf16(RMSNorm(x_residual)) in the combine pass. h_next may alias h."""
+    import ctypes
+
+    torch = _torch()
+    cfg = _rr.RerouteConfig(retain_count, threshold)
+    T, K = int(ids.shape[0]), int(ids.shape[1])
+    dsim = _rr.as_device_sim(sim, bank.device)
+    dev = bank.device
+    if out is None:
+        rr = _rr.DeviceReroute(
+            new_indices=torch.empty((T, K), dtype=torch.int32, device=dev),
+            expert_class=torch.empty(bank.M, dtype=torch.uint8, device=dev),
+            reroute_map=torch.empty(bank.M, dtype=torch.int32, device=dev),
+            active_list=torch.empty(bank.M, dtype=torch.int32, device=dev),
+            n_active=torch.empty(1, dtype=torch.int32, device=dev),
+            status=torch.zeros(1, dtype=torch.int32, device=dev),
+        )
+        y = torch.empty((T, bank.d_h), dtype=torch.float32, device=dev) if want_y else None
+        out = LayerOutput(y, None, rr.status, rr)
+    rr = out.reroute
+    flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    _lib.call("sere_moe_block_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
+              activation_code(activation), dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags,
+              h.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, rr.new_indices.data_ptr(),
+              rr.expert_class.data_ptr(), rr.reroute_map.data_ptr(), rr.active_list.data_ptr(),
+              rr.n_active.data_ptr(), x_residual.data_ptr(), h_next.data_ptr(), ctypes.c_float(eps),
+              out.y.data_ptr() if out.y is not None else None, ws.data_ptr(), ws.numel(), out.status.data_ptr(),
+              _stream_ptr(stream))
+    dsim.validated = True
+    return out
+
+
 def moe_forward_ep_device(bank: ExpertBank, n_experts: int, expert_lo: int, sim, retain_count: int,
                           threshold: float, x, ids, weights, activation: str = "silu", stream=None,
                           out: LayerOutput | None = None) -> LayerOutput:
@@ -304,16 +341,26 @@ def moe_forward_ep_device(bank: ExpertBank, n_experts: int, expert_lo: int, sim,
     return out
 
 
-def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False, bias=None, out=None):
-    """moe.py:268-277 on CUDA: w_router bf16 [d_h,M], x bf16 [T,d_h] -> (ids int32, weights f32[, logits]).
+_ROUTE_WS: dict = {}
+
+
+def router_weight_t(w_router):
+    """RouterWeights.w_router [d_h, M] -> the kernel's expert-major bf16 [M, d_h] (done once per layer)."""
+    torch = _torch()
+    return w_router.to(torch.bfloat16).t().contiguous()
+
+
+def route_topk_device(w_router_t, x, top_k: int, stream=None, logits: bool = False, bias=None, out=None):
+    """moe.py:268-277 on CUDA: w_router_t bf16 [M, d_h] (see `router_weight_t`), x bf16 [T,d_h]
+    -> (ids int32 [T,K], weights f32 [T,K][, logits f32 [T,M]]).
     `bias` (f32 [M], optional) is the benchmark's popularity-skew knob added to the logits."""
     torch = _torch()
     x = x.to(torch.bfloat16).contiguous()
-    w = w_router.to(torch.bfloat16).contiguous()
+    w = w_router_t.to(torch.bfloat16).contiguous()
     T, d_h = int(x.shape[0]), int(x.shape[1])
-    if w.shape[0] != d_h:
-        raise DimensionError(f"input width {d_h} does not match router d_h {w.shape[0]}")
-    M = int(w.shape[1])
+    if w.shape[1] != d_h:
+        raise DimensionError(f"input width {d_h} does not match router d_h {w.shape[1]}")
+    M = int(w.shape[0])
     if not 1 <= top_k <= M:
         raise ConfigError(f"top_k must satisfy 1 <= K <= M (got K={top_k}, M={M})")
     if out is not None:
@@ -323,9 +370,15 @@ def route_topk_device(w_router, x, top_k: int, stream=None, logits: bool = False
         wts = torch.empty((T, top_k), dtype=torch.float32, device=x.device)
     lg = torch.empty((T, M), dtype=torch.float32, device=x.device) if logits else None
     b = bias.to(torch.float32).contiguous() if bias is not None else None
+    nbytes = _lib.load().sere_route_workspace_bytes(T, d_h, M)
+    key = str(x.device)
+    ws = _ROUTE_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=x.device)  # tickets start at zero
+        _ROUTE_WS[key] = ws
     _lib.call("sere_route_topk", x.data_ptr(), w.data_ptr(), b.data_ptr() if b is not None else None,
-              T, d_h, M, int(top_k), ids.data_ptr(),
-              wts.data_ptr(), lg.data_ptr() if lg is not None else None, _stream_ptr(stream))
+              T, d_h, M, int(top_k), ids.data_ptr(), wts.data_ptr(), lg.data_ptr() if lg is not None else None,
+              ws.data_ptr(), ws.numel(), _stream_ptr(stream))
     return (ids, wts, lg) if logits else (ids, wts)
 
 
@@ -417,7 +470,7 @@ def route_topk(router: Any, x: Any) -> Assignment:
     dev = torch.device("cuda", torch.cuda.current_device())
     w = torch.as_tensor(np.asarray(router.w_router, dtype=np.float32)).to(dev)
     xt = torch.as_tensor(np.asarray(x, dtype=np.float32)).to(dev)
-    ids, wts = route_topk_device(w, xt, int(router.top_k))
+    ids, wts = route_topk_device(router_weight_t(w), xt, int(router.top_k))
     return Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
 
 
@@ -449,7 +502,7 @@ def model_forward(model: Any, batch: Any, config: Any = None, sims: Sequence | N
             original = a
         else:
             wr = torch.as_tensor(np.asarray(layer.router.w_router, dtype=np.float32)).to(dev)
-            ids, wts = route_topk_device(wr, x, int(layer.router.top_k))
+            ids, wts = route_topk_device(router_weight_t(wr), x, int(layer.router.top_k))
             original = Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
         if apply_rewrite:
             dsim = _rr._cached_sim(sims[l], dev)

@@ -22,7 +22,7 @@ def test_router_matches_fp64_topk_on_same_inputs(cuda_device):
     exceeds the fp32 accumulation error; softmax weights within 1e-5."""
     import torch
 
-    from paper_2602_07616_b200.moe import route_topk_device
+    from paper_2602_07616_b200.moe import route_topk_device, router_weight_t
 
     for (T, d_h, M, K) in [(512, 2048, 128, 8), (256, 4096, 8, 2), (256, 2048, 64, 6), (7, 24, 5, 2)]:
         g = torch.Generator(device="cuda")
@@ -30,7 +30,7 @@ def test_router_matches_fp64_topk_on_same_inputs(cuda_device):
         x = torch.randn(T, d_h, device="cuda", generator=g).to(torch.bfloat16)
         w = (torch.randn(d_h, M, device="cuda", generator=g) / d_h ** 0.5).to(torch.bfloat16)
         bias = torch.randn(M, device="cuda", generator=g)
-        ids, wts, lg = route_topk_device(w, x, K, logits=True, bias=bias)
+        ids, wts, lg = route_topk_device(router_weight_t(w), x, K, logits=True, bias=bias)
         logits64 = x.double().cpu().numpy() @ w.double().cpu().numpy() + bias.double().cpu().numpy()[None, :]
         np.testing.assert_allclose(lg.double().cpu().numpy(), logits64, atol=2e-4, rtol=1e-4)
         ref_ids, ref_w = O.topk_softmax(logits64, K)
