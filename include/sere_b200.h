@@ -195,6 +195,10 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
  * n == 0 disables. */
 int sere_set_stage_events(void* const* events, int n);
 
+/* Debug: when non-NULL, the re-routing/align kernel writes clock64() after each of its
+ * barrier-separated phases into dev_buf[0..15] (device int64). NULL disables. */
+int sere_debug_set_align_clocks(int64_t* dev_buf);
+
 /* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).
  * ------------------------------------------------------------------------ */

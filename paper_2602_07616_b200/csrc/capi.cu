@@ -15,7 +15,7 @@ namespace sere {
 namespace {
 
 constexpr int kMaxCells = 16384;  // T*K limit of the single-CTA align kernel (u16 counters, 64 KB ids)
-constexpr int kMaxExperts = 1024;
+constexpr int kMaxExperts = 256;  // smem of the single-CTA align kernel (per-warp expert masks)
 constexpr int kMaxShared = 31;
 
 int g_num_sms[64] = {0};
@@ -33,6 +33,8 @@ int num_sms() {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+long long* g_align_dbg = nullptr;  // sere_debug_set_align_clocks
 
 constexpr int kStageEvents = 6;
 thread_local cudaEvent_t t_stage_events[kStageEvents];
@@ -143,6 +145,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.units_dn_per = d.tiles_dn * d.ksplit_dn;
   ap.e_lo = e_lo;
   ap.m_local = m_local;
+  ap.dbg = g_align_dbg;
   stage_mark(0, stream);
   cudaError_t e = launch_reroute_align(ap, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -239,6 +242,7 @@ int sere_reroute(const int32_t* ids_in, const double* sim, int T, int K, int M, 
   ap.mode = MODE_REROUTE;
   ap.e_lo = 0;
   ap.m_local = M;
+  ap.dbg = g_align_dbg;
   ap.ids_out = ids_out;
   ap.expert_class = expert_class;
   ap.reroute_map = reroute_map;
@@ -403,6 +407,11 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
   if (!x || !h_out) return SERE_ERR_DIMENSION;
   return check_cuda(launch_residual_rmsnorm(x, y, reinterpret_cast<__nv_bfloat16*>(h_out), T, d_h, eps,
                                             static_cast<cudaStream_t>(stream)));
+}
+
+int sere_debug_set_align_clocks(int64_t* dev_buf) {
+  g_align_dbg = reinterpret_cast<long long*>(dev_buf);
+  return SERE_OK;
 }
 
 int sere_set_stage_events(void* const* events, int n) {

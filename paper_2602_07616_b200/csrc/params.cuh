@@ -31,6 +31,7 @@ struct AlignParams {
   int tiles_gu;      // gate/up units per column block
   int units_dn_per;  // down units per column block (tiles_dn * ksplit_dn)
   int e_lo, m_local; // expert-parallel ownership: bank holds global experts [e_lo, e_lo+m_local)
+  long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
 };
 
 struct GemmParams {

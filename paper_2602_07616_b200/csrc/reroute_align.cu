@@ -10,9 +10,10 @@
 //      (rerouting.py:160) and the per-cell rewrite of slots >= S;
 //  (2) count/align for the grouped FFN: per-expert counts over the (rewritten)
 //      table, groups = active experts ascending then shared experts, each padded
-//      to 16 rows; a STABLE (token, slot)-ordered rank inside each group from a
-//      two-pass warp __match_any_sync count, giving slot_row[t,k] and the inverse
-//      row_token[row]; work-unit prefixes for both grouped GEMMs.
+//      to 16 rows; a deterministic rank inside each group (rows ordered by token
+//      block, slot, token) from per-warp smem token masks + popc, giving
+//      slot_row[t,k] and the inverse row_token[row]; work-unit prefixes for both
+//      grouped GEMMs. Threads own whole token rows (no div/mod by K).
 // Everything is integer / fp64-compare work on <= 16K cells: latency-bound, so a
 // single CTA with no global round trips between phases is the fastest shape.
 #include <cuda_runtime.h>
@@ -27,17 +28,20 @@ namespace sere {
 
 constexpr int kAlignThreads = 1024;
 constexpr int kAlignWarps = kAlignThreads / 32;
+constexpr int kTokBlk = 32;  // tokens per warp block in the rank pass (lane = token)
+#define SERE_PHASE(i) do { if (p.dbg && threadIdx.x == 0) p.dbg[(i)] = clock64(); } while (0)
 
 // M = global expert count (ids, sim, classes); Et = local groups (bank experts + shared)
 __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) {
-  const int TK = T * K, MW = (M + 31) / 32;
+  const int TK = T * K, TB = (T + kTokBlk - 1) / kTokBlk;
   size_t b = 0;
-  b += static_cast<size_t>(TK) * 4;          // s_ids
-  b += static_cast<size_t>(MW) * 4 * 2;      // s_h, s_need
-  b += static_cast<size_t>(M) * 4 * 2;       // s_map, s_list
-  b += static_cast<size_t>(Et) * 4 * 3;      // s_cnt, s_row0, s_gidx
-  b += static_cast<size_t>(round_up(M, 4));  // s_cls
-  b += static_cast<size_t>(kAlignWarps) * Et * 2;  // s_wc
+  b += static_cast<size_t>(TK) * 4;                   // s_ids
+  b += static_cast<size_t>(M) * 4 * 2;                // s_map, s_list
+  b += static_cast<size_t>(Et) * 4 * 2;               // s_cnt, s_row0
+  b += static_cast<size_t>(kAlignWarps) * Et * 4;     // s_bm (per-warp token masks)
+  b += static_cast<size_t>(round_up(TK, 2)) * 2;      // s_rk
+  b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb
+  b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_need, s_cls
   return round_up(static_cast<int>(b), 16);
 }
 
@@ -54,36 +58,60 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int T = p.T, K = p.K, M = p.M, S = p.S;
-  const int TK = T * K, MW = (M + 31) / 32;
+  const int TK = T * K, TB = (T + kTokBlk - 1) / kTokBlk;
   const int e_lo = p.e_lo, m_loc = p.m_local, Et = m_loc + p.n_shared;  // expert-parallel ownership
   int32_t* s_ids = reinterpret_cast<int32_t*>(smem);
-  uint32_t* s_h = reinterpret_cast<uint32_t*>(s_ids + TK);
-  uint32_t* s_need = s_h + MW;
-  int32_t* s_map = reinterpret_cast<int32_t*>(s_need + MW);
-  int32_t* s_list = s_map + M;  // compact list of needed secondaries
-  int32_t* s_cnt = s_list + M;
-  int32_t* s_row0 = s_cnt + Et;
-  int32_t* s_gidx = s_row0 + Et;
-  uint8_t* s_cls = reinterpret_cast<uint8_t*>(s_gidx + Et);
-  uint16_t* s_wc = reinterpret_cast<uint16_t*>(s_cls + round_up(M, 4));
-  __shared__ int s_err_id, s_err_sim, s_err_route;
+  int32_t* s_map = s_ids + TK;
+  int32_t* s_list = s_map + M;   // compact list of needed secondaries
+  int32_t* s_cnt = s_list + M;   // per bank-expert totals
+  int32_t* s_row0 = s_cnt + Et;  // first permuted row of each bank expert's group
+  uint32_t* s_bm = reinterpret_cast<uint32_t*>(s_row0 + Et);          // [warps][Et]
+  uint16_t* s_rk = reinterpret_cast<uint16_t*>(s_bm + kAlignWarps * Et);  // [TK] rank inside token block
+  uint16_t* s_cntb = s_rk + round_up(TK, 2);                             // [TB][Et] counts -> prefixes
+  uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
+  uint8_t* s_need = s_hflag + round_up(M, 4);
+  uint8_t* s_cls = s_need + round_up(M, 4);
+  __shared__ int s_err_id, s_err_sim, s_err_route, s_nneed;
 
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
   const bool reroute = (p.mode & MODE_REROUTE) != 0;
   const bool align = (p.mode & MODE_ALIGN) != 0;
+  const int s_eff = S < K ? S : K;  // S == K: identity re-routing, every routed expert is primary
+  auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
 
   if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; }
-  for (int i = tid; i < MW; i += nthr) { s_h[i] = 0u; s_need[i] = 0u; }
-  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; }
-  for (int e = tid; e < Et; e += nthr) s_cnt[e] = 0;
+  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
+  if (align) {
+    for (int i = tid; i < kAlignWarps * Et; i += nthr) s_bm[i] = 0u;
+    for (int i = tid; i < TB * Et; i += nthr) s_cntb[i] = 0;
+  }
   __syncthreads();
+  SERE_PHASE(0);
 
-  // ---- load + validate ids (rerouting.py:111-114 / moe.py:299-300)
-  for (int c = tid; c < TK; c += nthr) {
-    const int v = p.ids_in[c];
-    s_ids[c] = v;
-    if (v < 0 || v >= M) s_err_id = 1;
+  // ---- load + validate ids (rerouting.py:111-114 / moe.py:299-300); lane = token, no div/mod
+  const bool vec = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(p.ids_in) & 15) == 0;
+  // s_ids is column-major [K][T] so that lane = token accesses are bank-conflict free
+  for (int t = tid; t < T; t += nthr) {
+    const int32_t* src = p.ids_in + static_cast<size_t>(t) * K;
+    bool bad = false;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      int v4[4];
+      if (vec) {
+        const int4 q = __ldg(reinterpret_cast<const int4*>(src + k0));
+        v4[0] = q.x; v4[1] = q.y; v4[2] = q.z; v4[3] = q.w;
+      } else {
+        for (int j = 0; j < 4; ++j) v4[j] = k0 + j < K ? __ldg(src + k0 + j) : 0;
+      }
+      for (int j = 0; j < 4 && k0 + j < K; ++j) {
+        const int k = k0 + j, v = v4[j];
+        s_ids[k * T + t] = v;
+        const bool ok = v >= 0 && v < M;
+        bad |= !ok;
+        if (reroute && ok && k < s_eff) s_hflag[v] = 1;  // primary set H (rerouting.py:147; Alg. 2 l.467-471)
+      }
+    }
+    if (bad) s_err_id = 1;
   }
   if (reroute && (p.flags & SERE_FLAG_CHECK_SIM)) {  // rerouting.py:115-116 (NaN passes, as there)
     for (int i = tid; i < M * M; i += nthr) {
@@ -92,6 +120,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     }
   }
   __syncthreads();
+  SERE_PHASE(1);
   if (s_err_id || s_err_sim) {
     if (tid == 0) {
       const int code = s_err_id ? (reroute ? SERE_ERR_DIMENSION : SERE_ERR_ROUTING) : SERE_ERR_INPUT;
@@ -102,43 +131,34 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
 
   if (reroute) {
-    // ---- primary mask H (rerouting.py:147; Alg. 2).  S == K: identity, all primary.
-    const int s_eff = S < K ? S : K;
-    for (int c = tid; c < TK; c += nthr) {
-      if ((c % K) < s_eff) {
-        const int e = s_ids[c];
-        atomicOr(&s_h[e >> 5], 1u << (e & 31));
-      }
-    }
-    __syncthreads();
-    // ---- distinct secondary experts of slots >= S that are not primary (rerouting.py:152-156)
-    if (S < K) {
-      for (int c = tid; c < TK; c += nthr) {
-        if ((c % K) >= S) {
-          const int e = s_ids[c];
-          if (!((s_h[e >> 5] >> (e & 31)) & 1u)) atomicOr(&s_need[e >> 5], 1u << (e & 31));
+    // ---- distinct secondaries: experts of slots >= S that are not primary (rerouting.py:152-156)
+    if (S < K)
+      for (int t = tid; t < T; t += nthr)
+        for (int k = S; k < K; ++k) {
+          const int e = s_ids[k * T + t];
+          if (!s_hflag[e]) s_need[e] = 1;
         }
-      }
-    }
     __syncthreads();
-    // ---- compact list of the needed secondaries (ascending)
-    __shared__ int s_nneed;
-    if (warp == 0) {
+    SERE_PHASE(2);
+    if (warp == 0) {  // ascending compact list of the secondaries
       int base = 0;
       for (int c0 = 0; c0 < M; c0 += 32) {
         const int e = c0 + lane;
-        const bool nd = e < M && ((s_need[e >> 5] >> (e & 31)) & 1u);
+        const bool nd = e < M && s_need[e];
         const unsigned m = __ballot_sync(0xffffffffu, nd);
         if (nd) s_list[base + __popc(m & ((1u << lane) - 1u))] = e;
         base += __popc(m);
       }
       if (lane == 0) s_nneed = base;
     }
+    for (int e = tid; e < M; e += nthr)
+      if (s_hflag[e]) s_cls[e] = SERE_CLASS_PRIMARY;
     __syncthreads();
+    SERE_PHASE(3);
     // ---- per-secondary argmax over the primary set (rerouting.py:78-97,157-164): one 16-lane
     // group per secondary u; every lane first issues all its loads of row u (independent, so
     // they overlap), then compares ascending with strict '>' and the group reduces to the
-    // first maximum (larger value, then lower index).
+    // first maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
     const int n_need = s_nneed;
     const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
     for (int base = 0; base < n_need; base += ngrp) {
@@ -159,7 +179,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int v = v0 + glane + 16 * j;
-            if (v < M && ((s_h[v >> 5] >> (v & 31)) & 1u) && vals[j] > bs) { bs = vals[j]; bi = v; }
+            if (v < M && s_hflag[v] && vals[j] > bs) { bs = vals[j]; bi = v; }
           }
         }
       }
@@ -178,22 +198,33 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         }
       }
     }
-    for (int e = tid; e < M; e += nthr)
-      if ((s_h[e >> 5] >> (e & 31)) & 1u) s_cls[e] = SERE_CLASS_PRIMARY;
     __syncthreads();
-    // ---- rewrite the secondary cells (weights are never touched)
-    if (S < K) {
-      for (int c = tid; c < TK; c += nthr) {
-        if ((c % K) >= S) {
-          const int e = s_ids[c];
-          if (s_cls[e] & SERE_CLASS_REROUTED) s_ids[c] = s_map[e];
+    SERE_PHASE(4);
+    // ---- rewrite the secondary cells (weights are never touched) + outputs
+    bool bad = false;
+    const bool vec_out = vec && (reinterpret_cast<uintptr_t>(p.ids_out) & 15) == 0;
+    for (int t = tid; t < T; t += nthr) {
+      for (int k = S; k < K; ++k) {
+        const int e = s_ids[k * T + t];
+        if (s_cls[e] & SERE_CLASS_REROUTED) {
+          const int v = s_map[e];
+          s_ids[k * T + t] = v;
+          bad |= (v < 0 || v >= M);  // reference NaN quirk: a secondary mapped to -1
+        }
+      }
+      if (p.ids_out) {
+        int32_t* dst = p.ids_out + static_cast<size_t>(t) * K;
+        for (int k0 = 0; k0 < K; k0 += 4) {
+          if (vec_out) {
+            *reinterpret_cast<int4*>(dst + k0) = make_int4(s_ids[k0 * T + t], s_ids[(k0 + 1) * T + t],
+                                                           s_ids[(k0 + 2) * T + t], s_ids[(k0 + 3) * T + t]);
+          } else {
+            for (int k = k0; k < K && k < k0 + 4; ++k) dst[k] = s_ids[k * T + t];
+          }
         }
       }
     }
-    __syncthreads();
-    // ---- outputs
-    if (p.ids_out)
-      for (int c = tid; c < TK; c += nthr) p.ids_out[c] = s_ids[c];
+    if (bad) s_err_route = 1;
     if (p.expert_class)
       for (int e = tid; e < M; e += nthr) p.expert_class[e] = s_cls[e];
     if (p.reroute_map)
@@ -212,138 +243,155 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         if (p.plan) p.plan[P_NACTIVE] = base;
       }
     }
+    __syncthreads();
+    SERE_PHASE(5);
   }
 
   if (!align) {
     if (tid == 0 && p.status_dev) *p.status_dev = SERE_OK;
     return;
   }
+  // the rewritten table may hold -1 (reference NaN quirk at rho == 0): layer_forward then
+  // raises RoutingError (moe.py:299-300)
+  if (s_err_route) {
+    if (tid == 0) {
+      if (p.status_dev) *p.status_dev = SERE_ERR_ROUTING;
+      p.plan[P_STATUS] = SERE_ERR_ROUTING;
+    }
+    return;
+  }
 
   // ================================================================ count/align
-  // the rewritten table may hold -1 (reference NaN quirk at rho == 0): layer_forward
-  // then raises RoutingError (moe.py:299-300)
-  if (reroute) {
-    for (int c = tid; c < TK; c += nthr) {
-      const int v = s_ids[c];
-      if (v < 0 || v >= M) s_err_route = 1;
-    }
-    __syncthreads();
-    if (s_err_route) {
-      if (tid == 0) {
-        if (p.status_dev) *p.status_dev = SERE_ERR_ROUTING;
-        p.plan[P_STATUS] = SERE_ERR_ROUTING;
+  // Rows of a group are ordered by (token block of 32, slot k, token): deterministic and
+  // computable without sorting. Pass 1, one warp per token block, lane = token: for each
+  // slot k every lane ORs its bit into the warp's mask of its expert; the cell's rank in
+  // the block is the block's running count of that expert + popc(mask & lanes below), and
+  // the lowest lane of each mask advances the running count. Counts never leave smem.
+  {
+    uint32_t* bm = s_bm + warp * Et;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int tb = warp; tb < TB; tb += nwarps) {
+      const int t = tb * kTokBlk + lane;
+      uint16_t* run = s_cntb + tb * Et;
+      for (int k = 0; k < K; ++k) {
+        const int el = t < T ? local_of(s_ids[k * T + t]) : -1;
+        if (el >= 0) atomicOr(&bm[el], 1u << lane);
+        __syncwarp();
+        unsigned m = 0;
+        if (el >= 0) {
+          m = bm[el];
+          s_rk[k * T + t] = static_cast<uint16_t>(run[el] + __popc(m & lt));
+        }
+        __syncwarp();
+        if (el >= 0 && lane == __ffs(m) - 1) {
+          run[el] = static_cast<uint16_t>(run[el] + __popc(m));
+          bm[el] = 0u;
+        }
+        __syncwarp();
       }
-      return;
     }
   }
-  // cells routed to experts this bank does not own (expert parallelism) take no row
-  auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
-  for (int c = tid; c < TK; c += nthr) {
-    const int el = local_of(s_ids[c]);
-    if (el >= 0) atomicAdd(&s_cnt[el], 1);
-  }
-  for (int s = tid; s < p.n_shared; s += nthr) s_cnt[m_loc + s] = T;
   __syncthreads();
+  SERE_PHASE(6);
+  // block counts -> exclusive prefixes over blocks; totals per bank expert
+  for (int e = tid; e < Et; e += nthr) {
+    if (e < m_loc) {
+      int run = 0;
+      for (int tb = 0; tb < TB; ++tb) {
+        const int v = s_cntb[tb * Et + e];
+        s_cntb[tb * Et + e] = static_cast<uint16_t>(run);
+        run += v;
+      }
+      s_cnt[e] = run;
+    } else {
+      s_cnt[e] = T;  // shared experts: every token (moe.py:308-309)
+    }
+  }
+  __syncthreads();
+  SERE_PHASE(7);
 
   const PlanOffsets po = plan_offsets(Et);
   int32_t* plan = p.plan;
-  if (warp == 0) {
-    int g_base = 0, row_base = 0, ugu_base = 0, udn_base = 0;
-    for (int c0 = 0; c0 < Et; c0 += 32) {
-      const int e = c0 + lane;
-      const int cnt = e < Et ? s_cnt[e] : 0;
-      const bool act = cnt > 0;
+  // group layout: groups = bank experts with cells (ascending) then shared experts; each
+  // padded to 16 rows. One warp per chunk of 32 experts scans in parallel, then every
+  // chunk adds the totals of the chunks before it.
+  __shared__ int s_tot[4][40];
+  const int nch = (Et + 31) / 32;
+  {
+    const int e = warp * 32 + lane;
+    int cnt = 0, pad = 0, ugu = 0, udn = 0, gi = 0, r_in = 0, gu_in = 0, dn_in = 0;
+    bool act = false;
+    if (warp < nch) {
+      cnt = e < Et ? s_cnt[e] : 0;
+      act = cnt > 0;
       const unsigned m = __ballot_sync(0xffffffffu, act);
-      const int gi = g_base + __popc(m & ((1u << lane) - 1u));
-      const int pad = round_up(cnt, kRowAlign);
+      gi = __popc(m & ((1u << lane) - 1u));
+      pad = round_up(cnt, kRowAlign);
       const int ncb = (pad + kColBlock - 1) / kColBlock;
-      const int ugu = p.tiles_gu * ncb, udn = p.units_dn_per * ncb;
-      const int r_incl = warp_incl_scan(pad);
-      const int gu_incl = warp_incl_scan(ugu);
-      const int dn_incl = warp_incl_scan(udn);
+      ugu = p.tiles_gu * ncb;
+      udn = p.units_dn_per * ncb;
+      r_in = warp_incl_scan(pad);
+      gu_in = warp_incl_scan(ugu);
+      dn_in = warp_incl_scan(udn);
+      if (lane == 31) {
+        s_tot[0][warp] = __popc(m);
+        s_tot[1][warp] = r_in;
+        s_tot[2][warp] = gu_in;
+        s_tot[3][warp] = dn_in;
+      }
+    }
+    __syncthreads();
+    if (warp < nch) {
+      int gb = 0, rb = 0, gub = 0, dnb = 0;
+      for (int w = 0; w < warp; ++w) { gb += s_tot[0][w]; rb += s_tot[1][w]; gub += s_tot[2][w]; dnb += s_tot[3][w]; }
       if (e < Et) {
         if (act) {
-          plan[po.group_expert + gi] = e;
-          plan[po.group_row0 + gi] = row_base + r_incl - pad;
-          plan[po.group_rows + gi] = cnt;
-          plan[po.unit_off_gu + gi] = ugu_base + gu_incl - ugu;
-          plan[po.unit_off_dn + gi] = udn_base + dn_incl - udn;
-          s_row0[e] = row_base + r_incl - pad;
-          s_gidx[e] = gi;
-        } else {
-          s_row0[e] = -1;
-          s_gidx[e] = -1;
+          plan[po.group_expert + gb + gi] = e;
+          plan[po.group_row0 + gb + gi] = rb + r_in - pad;
+          plan[po.group_rows + gb + gi] = cnt;
+          plan[po.unit_off_gu + gb + gi] = gub + gu_in - ugu;
+          plan[po.unit_off_dn + gb + gi] = dnb + dn_in - udn;
         }
+        s_row0[e] = act ? rb + r_in - pad : -1;
         plan[po.counts + e] = cnt;
       }
-      g_base += __popc(m);
-      row_base += __shfl_sync(0xffffffffu, r_incl, 31);
-      ugu_base += __shfl_sync(0xffffffffu, gu_incl, 31);
-      udn_base += __shfl_sync(0xffffffffu, dn_incl, 31);
-    }
-    if (lane == 0) {
-      plan[P_NGROUPS] = g_base;
-      plan[P_TOTAL_ROWS] = row_base;
-      plan[P_UNITS_GU] = ugu_base;
-      plan[P_UNITS_DN] = udn_base;
-      plan[po.unit_off_gu + g_base] = ugu_base;
-      plan[po.unit_off_dn + g_base] = udn_base;
-      if (!reroute) plan[P_NACTIVE] = g_base - (p.n_shared > 0 ? p.n_shared : 0);
+      if (warp == nch - 1 && lane == 0) {
+        const int g_tot = gb + s_tot[0][warp], r_tot = rb + s_tot[1][warp];
+        const int gu_tot = gub + s_tot[2][warp], dn_tot = dnb + s_tot[3][warp];
+        plan[P_NGROUPS] = g_tot;
+        plan[P_TOTAL_ROWS] = r_tot;
+        plan[P_UNITS_GU] = gu_tot;
+        plan[P_UNITS_DN] = dn_tot;
+        plan[po.unit_off_gu + g_tot] = gu_tot;
+        plan[po.unit_off_dn + g_tot] = dn_tot;
+        if (!reroute) plan[P_NACTIVE] = g_tot - p.n_shared;
+      }
     }
   }
-  // zero the per-warp per-expert counters
-  for (int i = tid; i < nwarps * Et; i += nthr) s_wc[i] = 0;
   __syncthreads();
+  SERE_PHASE(8);
 
-  // ---- stable ranks: warp w owns cells [w*L, (w+1)*L) in (token, slot) order
-  const int L = (TK + nwarps - 1) / nwarps;
-  const int c_lo = warp * L, c_hi = min(TK, c_lo + L);
-  uint16_t* wc = s_wc + warp * Et;
-  for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-    const int c = c0 + lane;
-    const int el = c < c_hi ? local_of(s_ids[c]) : -1;
-    const int e = el >= 0 ? el : -1 - lane;  // unique sentinel for idle / foreign cells
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    if (el >= 0 && lane == __ffs(peers) - 1) wc[e] += static_cast<uint16_t>(__popc(peers));
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int e = tid; e < Et; e += nthr) {  // exclusive prefix over warps
-    int run = 0;
-    for (int w = 0; w < nwarps; ++w) {
-      const int v = s_wc[w * Et + e];
-      s_wc[w * Et + e] = static_cast<uint16_t>(run);
-      run += v;
+  // ---- pass 2: permuted row of every (token, slot) cell and its inverse
+  for (int t = tid; t < T; t += nthr) {
+    const int tb = t / kTokBlk;
+    for (int k = 0; k < K; ++k) {
+      const int c = t * K + k;
+      const int el = local_of(s_ids[k * T + t]);
+      if (el >= 0) {
+        const int row = s_row0[el] + s_cntb[tb * Et + el] + s_rk[k * T + t];
+        p.slot_row[c] = row;
+        p.row_token[row] = t;
+      } else {
+        p.slot_row[c] = -1;  // owned by another rank (expert parallelism): the combine skips it
+      }
+    }
+    for (int s = 0; s < p.n_shared; ++s) {  // shared experts: every token, in token order
+      const int row = s_row0[m_loc + s] + t;
+      p.slot_row[TK + t * p.n_shared + s] = row;
+      p.row_token[row] = t;
     }
   }
-  __syncthreads();
-  for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-    const int c = c0 + lane;
-    const int el = c < c_hi ? local_of(s_ids[c]) : -1;
-    const int e = el >= 0 ? el : -1 - lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    int base = 0;
-    if (el >= 0) base = wc[e];
-    __syncwarp();
-    if (el >= 0) {
-      const int row = s_row0[e] + base + __popc(peers & ((1u << lane) - 1u));
-      p.slot_row[c] = row;
-      p.row_token[row] = c / K;
-      if (lane == __ffs(peers) - 1) wc[e] = static_cast<uint16_t>(base + __popc(peers));
-    } else if (c < c_hi) {
-      p.slot_row[c] = -1;  // owned by another rank: the combine skips it
-    }
-    __syncwarp();
-  }
-  // shared experts: every token, in token order (moe.py:308-309)
-  for (int i = tid; i < T * p.n_shared; i += nthr) {
-    const int t = i / p.n_shared, s = i % p.n_shared;
-    const int row = s_row0[m_loc + s] + t;
-    p.slot_row[TK + i] = row;
-    p.row_token[row] = t;
-  }
-  // padding rows of each group
-  for (int e = warp; e < Et; e += nwarps) {
+  for (int e = warp; e < Et; e += nwarps) {  // padding rows of each group
     const int cnt = s_cnt[e];
     if (cnt == 0) continue;
     const int pad = round_up(cnt, kRowAlign);

@@ -1,0 +1,62 @@
+"""Phase timing of the re-routing/align kernel (clock64 after each barrier phase).
+
+    python -m paper_2602_07616_b200.debug_align [--T 512 --M 128 --K 8]
+"""
+
+from __future__ import annotations
+
+import argparse
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--T", type=int, default=512)
+    ap.add_argument("--M", type=int, default=128)
+    ap.add_argument("--K", type=int, default=8)
+    ap.add_argument("--beta", type=float, default=1.0)
+    a = ap.parse_args()
+
+    import numpy as np
+    import torch
+
+    from . import _lib, build
+    from .decode import uniform_sim
+    from .rerouting import DeviceSimilarity, reroute
+
+    build.build()
+    T, M, K = a.T, a.M, a.K
+    logits = torch.randn(T, M, device="cuda") + a.beta * torch.randn(M, device="cuda")
+    ids = torch.topk(logits, K, dim=1).indices.to(torch.int32)
+    sim = DeviceSimilarity(uniform_sim(np.random.default_rng(0), M))  # validated once, like the decode step
+    dbg = torch.zeros(16, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        reroute(ids, sim, 1, 0.5).check()
+    _lib.load().sere_debug_set_align_clocks(dbg.data_ptr())
+    reroute(ids, sim, 1, 0.5).check()
+    torch.cuda.synchronize()
+    _lib.load().sere_debug_set_align_clocks(None)
+    c = dbg.cpu().numpy()
+    n = int((c > 0).sum())
+    d = np.diff(c[:n])
+    print("reroute-only phases (cycles):", d.tolist(), "total", int(c[n - 1] - c[0]))
+
+    from .moe import ExpertBank, moe_forward_device
+
+    bank = ExpertBank.random(M, 0, 256, 128, seed=0)  # small dims: only the align kernel matters here
+    x = torch.randn(T, 256, device="cuda").to(torch.bfloat16)
+    w = torch.full((T, K), 1.0 / K, device="cuda")
+    for _ in range(3):
+        moe_forward_device(bank, sim, 1, 0.5, x, ids, w).check()
+    dbg.zero_()
+    _lib.load().sere_debug_set_align_clocks(dbg.data_ptr())
+    moe_forward_device(bank, sim, 1, 0.5, x, ids, w).check()
+    torch.cuda.synchronize()
+    _lib.load().sere_debug_set_align_clocks(None)
+    c = dbg.cpu().numpy()
+    n = int((c > 0).sum())
+    d = np.diff(c[:n])
+    print("reroute+align phases (cycles):", d.tolist(), "total", int(c[n - 1] - c[0]))
+
+
+if __name__ == "__main__":
+    main()

@@ -99,7 +99,7 @@ def test_align_plan_integer_exact(cuda_device):
     from paper_2602_07616_b200 import _lib
     from paper_2602_07616_b200.moe import ExpertBank, layer_forward_device, workspace
 
-    M, ns, d_h, d_m, T, K = 16, 2, 128, 64, 37, 4
+    M, ns, d_h, d_m, T, K = 16, 2, 128, 64, 77, 4
     bank = ExpertBank.random(M, ns, d_h, d_m, seed=1)
     rng = np.random.default_rng(2)
     ids = np.stack([rng.choice(M, K, replace=False) for _ in range(T)])
@@ -127,10 +127,11 @@ def test_align_plan_integer_exact(cuda_device):
     row0 = np.concatenate([[0], np.cumsum(pads)[:-1]])
     np.testing.assert_array_equal(plan[L.plan_group_row0_off:L.plan_group_row0_off + len(groups)], row0)
     assert plan[2] == sum(pads)
-    # stable (token, slot) order inside each group
+    # deterministic order inside each group: (token block of 32, slot, token)
     for gi, e in enumerate(groups):
         if e < M:
-            cells = [(t, k) for t in range(T) for k in range(K) if ids[t, k] == e]
+            cells = sorted([(t, k) for t in range(T) for k in range(K) if ids[t, k] == e],
+                           key=lambda c: (c[0] // 32, c[1], c[0]))
             rows = [slot_row[t * K + k] for (t, k) in cells]
         else:
             s = e - M
