@@ -365,12 +365,12 @@ def run_ours(args, wl):
         peak, peak_kind = measured_peak_hbm()
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "grouped_gemm_kernel (gate/up + down launches, tcgen05)",
+                "kernel": "moe_ffn_kernel (gate/up + down phases in one persistent tcgen05 launch)",
                 "peak_kind": peak_kind,
                 "bytes_per_layer_avg": float(bytes_layers.mean()),
                 "ffn_us_per_layer_avg": float(ffn_ms.mean() * 1e3),
                 "stage_us_per_layer_avg": {k: round(float(v) * 1e3, 2) for k, v in
-                                           zip(["reroute_align", "permute", "gate_up_gemm", "down_gemm", "combine"],
+                                           zip(["reroute_align", "permute", "ffn", "unused", "combine"],
                                                st.mean(axis=0))},
                 "ffn_share_of_layer_kernels": round(float(ffn_ms.sum() / st.sum()), 4),
                 "timing": f"CUDA events per stage, {stage_mode}, last of 3 steps"}

@@ -155,36 +155,26 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
-  const uint8_t* w2 = w13 + bank_w13_bytes(L.Et, d);
-  GemmParams gp{};
-  gp.a_base = w13;
-  gp.tiles_m = d.tiles_gu;
-  gp.ktiles = d.ktiles_gu;
-  gp.ksplit = 1;
-  gp.b_base = x_pack;
-  gp.r_max = L.r_max;
-  gp.plan = plan;
-  gp.Et = L.Et;
-  gp.which = 0;
-  gp.epi = 0;
-  gp.act = activation;
-  gp.h_pack = h_pack;
-  gp.y_perm = y_perm;
-  gp.d_h_pad = d.d_h_pad;
+  FfnParams fp{};
+  fp.w13 = w13;
+  fp.w2 = w13 + bank_w13_bytes(L.Et, d);
+  fp.tiles_gu = d.tiles_gu;
+  fp.ktiles_gu = d.ktiles_gu;
+  fp.tiles_dn = d.tiles_dn;
+  fp.ktiles_dn = d.ktiles_dn;
+  fp.ksplit_dn = d.ksplit_dn;
+  fp.x_pack = x_pack;
+  fp.h_pack = h_pack;
+  fp.y_perm = y_perm;
+  fp.r_max = L.r_max;
+  fp.d_h_pad = d.d_h_pad;
+  fp.plan = plan;
+  fp.Et = L.Et;
+  fp.act = activation;
   stage_mark(2, stream);
-  e = launch_grouped_gemm(gp, sms, stream);
+  e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
-
-  gp.a_base = w2;
-  gp.tiles_m = d.tiles_dn;
-  gp.ktiles = d.ktiles_dn;
-  gp.ksplit = d.ksplit_dn;
-  gp.b_base = h_pack;
-  gp.which = 1;
-  gp.epi = 1;
-  stage_mark(3, stream);
-  e = launch_grouped_gemm(gp, sms, stream);
-  if (e != cudaSuccess) return SERE_ERR_CUDA;
+  stage_mark(3, stream);  // gate/up and down run in one launch: stage 3 is empty
 
   stage_mark(4, stream);
   e = launch_combine(y_perm, d, L.r_max, plan, slot_row, weights, T, K, n_shared, y,

@@ -1,4 +1,5 @@
-// grouped_ffn.cu -- grouped expert GEMMs on the 5th-gen tensor cores (tcgen05).
+// grouped_ffn.cu -- the expert SwiGLU FFN of one MoE layer as ONE persistent kernel on
+// the 5th-gen tensor cores (tcgen05), gate/up and down phases fused.
 //
 // Decode-time MoE is expert-weight streaming: each active expert's weights are read
 // once per layer while only 8..256 tokens use them, so the kernel is built to keep
@@ -8,21 +9,29 @@
 //  * weights live in the bank as contiguous 16 KB pre-swizzled tiles, so one bulk
 //    async copy (TMA engine, cp.async.bulk) per k-step streams 16 KB at full DRAM
 //    burst length with an evict-first L2 policy; activations come from the grouped
-//    swizzled buffer written by permute (L2-resident, evict-last);
-//  * persistent CTAs (one per SM), static round-robin over work units
-//    (expert group, m-tile, k-split, column block) read from the device-side plan;
-//    the smem ring (6 x 32 KB slots) runs across unit boundaries so the stream
+//    swizzled buffers (L2-resident, evict-last);
+//  * persistent CTAs (one per SM) take work units from a global ticket counter:
+//    first every gate/up unit (expert group, 64-feature m-tile, column block), then
+//    every down unit (group, 128-feature m-tile, k-split, column block), groups in
+//    the plan's schedule order (padded rows descending = longest-processing-time
+//    first, since a unit's cost grows with its column count). A down unit waits,
+//    before its first copy, until every gate/up unit of its group has published h
+//    (per-group counters in the plan, release/acquire + async-proxy fences), so the
+//    down phase of the heavy groups overlaps the gate/up tail of the light ones and
+//    there is no grid-wide barrier and no second launch;
+//  * the smem ring (6 x 32 KB slots) runs across unit boundaries so the stream
 //    never drains; two TMEM accumulators (2 x 256 columns) let the epilogue of
-//    unit i overlap the MMAs of unit i+1;
+//    unit i overlap the MMAs of unit i+1; unit ids reach the MMA and epilogue warps
+//    through a 4-entry smem queue;
 //  * warp roles: warp 0 = producer (one lane), warp 1 = MMA issuer (one lane,
 //    also owns TMEM alloc), warps 2..5 = epilogue (TMEM lane quadrants 2,3,0,1).
 // Epilogues:
-//  * SWIGLU (gate/up GEMM): A rows interleave gate and up features in 16-row
-//    blocks (pack_w13_kernel), so one warp's TMEM quadrant holds gate (lanes 0-15)
-//    and up (lanes 16-31) of the same 16 features; h = act(g) * u via one
-//    shfl_xor, rounded to bf16, stored straight into the swizzled B layout of the
-//    down GEMM (moe.py:243-245);
-//  * STORE_F32 (down GEMM): fp32 expert outputs per (row, feature), coalesced.
+//  * gate/up: A rows interleave gate and up features in 16-row blocks
+//    (pack_w13_kernel), so one warp's TMEM quadrant holds gate (lanes 0-15) and up
+//    (lanes 16-31) of the same 16 features; h = act(g) * u via one shfl_xor, rounded
+//    to bf16, stored straight into the swizzled B layout of the down phase
+//    (moe.py:243-245);
+//  * down: fp32 expert outputs per (row, feature), coalesced.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -34,118 +43,155 @@ namespace sere {
 
 constexpr int kSlots = 6;
 constexpr int kSlotBytes = 32768;
-constexpr int kGemmThreads = 192;
+constexpr int kFfnThreads = 192;
 constexpr int kTmemCols = 512;
-constexpr int kMaxGroupsSmem = 1056;  // Et <= 1055 supported by the smem plan cache
+constexpr int kQueue = 4;
 
 struct Unit {
-  int expert, mt, ks, row0, n_mma, rows_valid, kt_begin, kt_end;
+  int dn, g, expert, mt, ks, row0, n_mma, rows_valid, kt_begin, kt_end, need;
 };
 
-struct __align__(16) GemmSmemTail {
+struct __align__(16) FfnSmemTail {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
+  uint64_t q_full[kQueue];
+  uint64_t q_empty[kQueue];
+  int32_t queue[kQueue];
   uint32_t tmem_base;
-  int32_t n_groups, n_units;
+  int32_t n_groups, units_gu, units_dn;
 };
 
-__host__ __device__ inline size_t gemm_smem_bytes(int Et) {
-  return 1024 /*align slack*/ + static_cast<size_t>(kSlots) * kSlotBytes + sizeof(GemmSmemTail) +
-         static_cast<size_t>(4) * (Et + 1) * sizeof(int32_t);
+// per-schedule-position copies of the plan (6 arrays of Et + 1)
+__host__ __device__ inline size_t ffn_smem_bytes(int Et) {
+  return 1024 /*align slack*/ + static_cast<size_t>(kSlots) * kSlotBytes + sizeof(FfnSmemTail) +
+         static_cast<size_t>(6) * (Et + 1) * sizeof(int32_t);
 }
 
-__device__ __forceinline__ Unit decode_unit(int u, int n_groups, const int32_t* s_uoff, const int32_t* s_exp,
-                                            const int32_t* s_row0, const int32_t* s_rows, int ksplit,
-                                            int ktiles) {
+struct SchedView {
+  const int32_t *uoff_gu, *uoff_dn, *gid, *gexp, *grow0, *grows;
+};
+
+__device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, const SchedView& v,
+                                            const FfnParams& p) {
+  Unit U;
+  U.dn = u >= units_gu;
+  if (U.dn) u -= units_gu;
+  const int32_t* uoff = U.dn ? v.uoff_dn : v.uoff_gu;
   int lo = 0, hi = n_groups - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (s_uoff[mid] <= u) lo = mid; else hi = mid - 1;
+    if (uoff[mid] <= u) lo = mid; else hi = mid - 1;
   }
-  const int g = lo;
-  const int local = u - s_uoff[g];
-  const int rows = s_rows[g];
+  const int local = u - uoff[lo];
+  const int rows = v.grows[lo];
   const int n16 = round_up(rows, kRowAlign);
   const int ncb = (n16 + kColBlock - 1) / kColBlock;
   const int nc = local % ncb;
   const int tmp = local / ncb;
-  Unit U;
+  const int ksplit = U.dn ? p.ksplit_dn : 1;
+  const int ktiles = U.dn ? p.ktiles_dn : p.ktiles_gu;
   U.ks = tmp % ksplit;
   U.mt = tmp / ksplit;
-  U.expert = s_exp[g];
+  U.g = v.gid[lo];
+  U.expert = v.gexp[lo];
   const int col0 = nc * kColBlock;
   U.n_mma = min(kColBlock, n16 - col0);
   U.rows_valid = min(kColBlock, rows - col0);
-  U.row0 = s_row0[g] + col0;
+  U.row0 = v.grow0[lo] + col0;
   const int kchunk = (ktiles + ksplit - 1) / ksplit;
   U.kt_begin = U.ks * kchunk;
   U.kt_end = min(ktiles, U.kt_begin + kchunk);
+  U.need = p.tiles_gu * ncb;  // gate/up units of this group (the down units' dependency)
   return U;
 }
 
 __device__ __forceinline__ float act_apply(float g, int act) {
-  if (act == 0) return g / (1.0f + __expf(-g));  // SiLU (moe.py:28-35)
-  if (act == 1) return fmaxf(g, 0.0f);           // ReLU (moe.py:38-39)
-  const float c = 0.7978845608028654f;           // GELU-tanh (moe.py:42-45)
+  if (act == 0) return g * __frcp_rn(1.0f + __expf(-g));  // SiLU (moe.py:28-35)
+  if (act == 1) return fmaxf(g, 0.0f);                     // ReLU (moe.py:38-39)
+  const float c = 0.7978845608028654f;                     // GELU-tanh (moe.py:42-45)
   return 0.5f * g * (1.0f + tanhf(c * (g + 0.044715f * g * g * g)));
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const GemmParams p) {
+__global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  GemmSmemTail* tail = reinterpret_cast<GemmSmemTail*>(smem + kSlots * kSlotBytes);
-  int32_t* s_uoff = reinterpret_cast<int32_t*>(tail + 1);
-  int32_t* s_exp = s_uoff + (p.Et + 1);
-  int32_t* s_row0 = s_exp + (p.Et + 1);
-  int32_t* s_rows = s_row0 + (p.Et + 1);
+  FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kSlots * kSlotBytes);
+  int32_t* s_arr = reinterpret_cast<int32_t*>(tail + 1);
+  const int E1 = p.Et + 1;
+  SchedView sv{s_arr, s_arr + E1, s_arr + 2 * E1, s_arr + 3 * E1, s_arr + 4 * E1, s_arr + 5 * E1};
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PlanOffsets po = plan_offsets(p.Et);
-  const int status = p.plan[P_STATUS];
+  int32_t* plan = p.plan;
+  const int status = plan[P_STATUS];
+  const int ng = status == 0 ? plan[P_NGROUPS] : 0;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kSlots; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tail->tmem_full[i], 1); mbar_init(&tail->tmem_empty[i], 4); }
+    for (int i = 0; i < kQueue; ++i) { mbar_init(&tail->q_full[i], 1); mbar_init(&tail->q_empty[i], 1 + 4); }
     fence_mbar_init();
-    const int ng = status == 0 ? p.plan[P_NGROUPS] : 0;
     tail->n_groups = ng;
-    tail->n_units = status == 0 ? p.plan[p.which == 0 ? P_UNITS_GU : P_UNITS_DN] : 0;
+    tail->units_gu = status == 0 ? plan[P_UNITS_GU] : 0;
+    tail->units_dn = status == 0 ? plan[P_UNITS_DN] : 0;
   }
   if (warp == 1) tmem_alloc(&tail->tmem_base, kTmemCols);
-  if (status == 0) {
-    const int ng = p.plan[P_NGROUPS];
-    const int32_t* uoff = p.plan + (p.which == 0 ? po.unit_off_gu : po.unit_off_dn);
-    for (int i = threadIdx.x; i <= ng; i += blockDim.x) {
-      s_uoff[i] = uoff[i];
-      if (i < ng) {
-        s_exp[i] = p.plan[po.group_expert + i];
-        s_row0[i] = p.plan[po.group_row0 + i];
-        s_rows[i] = p.plan[po.group_rows + i];
-      }
+  for (int i = threadIdx.x; i <= ng; i += blockDim.x) {
+    const_cast<int32_t*>(sv.uoff_gu)[i] = plan[po.unit_off_gu + i];
+    const_cast<int32_t*>(sv.uoff_dn)[i] = plan[po.unit_off_dn + i];
+    if (i < ng) {
+      const int g = plan[po.sched + i];
+      const_cast<int32_t*>(sv.gid)[i] = g;
+      const_cast<int32_t*>(sv.gexp)[i] = plan[po.group_expert + g];
+      const_cast<int32_t*>(sv.grow0)[i] = plan[po.group_row0 + g];
+      const_cast<int32_t*>(sv.grows)[i] = plan[po.group_rows + g];
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tail->tmem_base;
-  const int n_groups = tail->n_groups, n_units = tail->n_units;
+  const int n_groups = tail->n_groups, units_gu = tail->units_gu;
+  const int units_total = units_gu + tail->units_dn;
+  int32_t* dep = plan + po.dep;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===================== producer: bulk async copies into the slot ring
+      // ===================== producer: tickets -> unit queue; bulk async copies into the slot ring
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const Unit U = decode_unit(u, n_groups, s_uoff, s_exp, s_row0, s_rows, p.ksplit, p.ktiles);
-        const uint8_t* a_unit =
-            p.a_base + (static_cast<size_t>(U.expert) * p.tiles_m + U.mt) * p.ktiles * static_cast<size_t>(kTileBytes);
+      int slot = 0, qs = 0;
+      uint32_t phase = 0, qph = 0;
+      for (;;) {
+        const int u = units_total > 0 ? atomicAdd(plan + P_TICKET, 1) : 0;
+        const bool done = u >= units_total;
+        mbar_wait(&tail->q_empty[qs], qph ^ 1u);
+        tail->queue[qs] = done ? -1 : u;
+        mbar_arrive(&tail->q_full[qs]);
+        if (++qs == kQueue) { qs = 0; qph ^= 1u; }
+        if (done) break;
+        const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
+        const uint8_t* a_unit;
+        const uint8_t* b_base;
+        if (U.dn) {
+          // h of this group must be complete: every gate/up unit of the group published it
+          if (ld_acquire_gpu(dep + U.g) < U.need) {
+            while (ld_acquire_gpu(dep + U.g) < U.need) __nanosleep(64);
+          }
+          fence_proxy_async_global();
+          a_unit = p.w2 + (static_cast<size_t>(U.expert) * p.tiles_dn + U.mt) * p.ktiles_dn *
+                              static_cast<size_t>(kTileBytes);
+          b_base = p.h_pack;
+        } else {
+          a_unit = p.w13 + (static_cast<size_t>(U.expert) * p.tiles_gu + U.mt) * p.ktiles_gu *
+                               static_cast<size_t>(kTileBytes);
+          b_base = p.x_pack;
+        }
         const int n0 = min(U.n_mma, 128), n1 = U.n_mma - n0;
         for (int kt = U.kt_begin; kt < U.kt_end; ++kt) {
-          const uint8_t* b_src = p.b_base + (static_cast<size_t>(kt) * p.r_max + U.row0) * 128;
+          const uint8_t* b_src = b_base + (static_cast<size_t>(kt) * p.r_max + U.row0) * 128;
           mbar_wait(&tail->empty[slot], phase ^ 1u);
           uint8_t* sdst = smem + slot * kSlotBytes;
           mbar_arrive_expect_tx(&tail->full[slot], kTileBytes + n0 * 128);
@@ -165,11 +211,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const Gem
   } else if (warp == 1) {
     if (lane == 0) {
       // ===================== MMA issuer (single thread)
-      int slot = 0;
-      uint32_t phase = 0;
-      int iter = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
-        const Unit U = decode_unit(u, n_groups, s_uoff, s_exp, s_row0, s_rows, p.ksplit, p.ktiles);
+      int slot = 0, qs = 0, iter = 0;
+      uint32_t phase = 0, qph = 0;
+      for (;; ++iter) {
+        mbar_wait(&tail->q_full[qs], qph);
+        const int u = tail->queue[qs];
+        mbar_arrive(&tail->q_empty[qs]);
+        if (++qs == kQueue) { qs = 0; qph ^= 1u; }
+        if (u < 0) break;
+        const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
         const int buf = iter & 1;
         const uint32_t use = static_cast<uint32_t>(iter >> 1);
         mbar_wait(&tail->tmem_empty[buf], (use & 1u) ^ 1u);
@@ -214,15 +264,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const Gem
   } else {
     // ===================== epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
     const int q = warp & 3;
-    int iter = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
-      const Unit U = decode_unit(u, n_groups, s_uoff, s_exp, s_row0, s_rows, p.ksplit, p.ktiles);
+    int qs = 0, iter = 0;
+    uint32_t qph = 0;
+    for (;; ++iter) {
+      mbar_wait(&tail->q_full[qs], qph);
+      const int u = tail->queue[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tail->q_empty[qs]);
+      if (++qs == kQueue) { qs = 0; qph ^= 1u; }
+      if (u < 0) break;
+      const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
       const int buf = iter & 1;
       const uint32_t use = static_cast<uint32_t>(iter >> 1);
       mbar_wait(&tail->tmem_full[buf], use & 1u);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * 256;
-      if (p.epi == EPI_SWIGLU) {
+      if (!U.dn) {
         // lanes 0-15: gate of feature f, lanes 16-31: up of the same f
         const int f = 16 * q + (lane & 15);  // feature within the 64-feature tile == column of h tile
         const int chunk = f >> 3;
@@ -263,6 +320,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const Gem
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->tmem_empty[buf]);
+      if (!U.dn) {
+        // publish this unit's slice of h: the down units of the group (any SM) read it with
+        // bulk copies (async proxy) after acquiring the counter
+        fence_proxy_async_global();
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          atomicAdd(dep + U.g, 1);
+        }
+      }
     }
   }
 
@@ -272,19 +339,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) grouped_gemm_kernel(const Gem
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-cudaError_t launch_grouped_gemm(const GemmParams& p, int num_sms, cudaStream_t stream) {
-  const size_t smem = gemm_smem_bytes(p.Et);
+cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream) {
+  const size_t smem = ffn_smem_bytes(p.Et);
   static size_t configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(moe_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  grouped_gemm_kernel<<<num_sms, kGemmThreads, smem, stream>>>(p);
+  moe_ffn_kernel<<<num_sms, kFfnThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-size_t grouped_gemm_smem(int Et) { return gemm_smem_bytes(Et); }
+size_t moe_ffn_smem(int Et) { return ffn_smem_bytes(Et); }
 
 }  // namespace sere

@@ -34,18 +34,17 @@ struct AlignParams {
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
 };
 
-struct GemmParams {
-  const uint8_t* a_base;  // bank region: tile (expert, mt, kt) at ((expert*tiles_m+mt)*ktiles+kt)*16KB
-  int tiles_m, ktiles, ksplit;
-  const uint8_t* b_base;  // activations [ktiles][r_max][128 B]
-  int r_max;
-  const int32_t* plan;
+struct FfnParams {
+  const uint8_t* w13;  // gate/up tiles (expert, mt, kt) at ((expert*tiles_gu+mt)*ktiles_gu+kt)*16KB
+  const uint8_t* w2;   // down tiles   (expert, mt, kt) at ((expert*tiles_dn+mt)*ktiles_dn+kt)*16KB
+  int tiles_gu, ktiles_gu, tiles_dn, ktiles_dn, ksplit_dn;
+  const uint8_t* x_pack;  // gate/up B operand [ktiles_gu][r_max][128 B]
+  uint8_t* h_pack;        // SwiGLU out = down B operand [ktiles_dn][r_max][128 B]
+  float* y_perm;          // down out [ksplit_dn][r_max][d_h_pad]
+  int r_max, d_h_pad;
+  int32_t* plan;          // written by reroute_align; the ticket and dep counters are updated here
   int Et;
-  int which;  // 0 = gate/up units, 1 = down units
-  int epi, act;
-  uint8_t* h_pack;  // SWIGLU out [d_m_pad/64][r_max][128 B]
-  float* y_perm;    // STORE_F32 out [ksplit][r_max][d_h_pad]
-  int d_h_pad;
+  int act;
 };
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
@@ -58,8 +57,8 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
                            cudaStream_t stream);
-cudaError_t launch_grouped_gemm(const GemmParams& p, int num_sms, cudaStream_t stream);
-size_t grouped_gemm_smem(int Et);
+cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream);
+size_t moe_ffn_smem(int Et);
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
                               int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out,
                               cudaStream_t stream);

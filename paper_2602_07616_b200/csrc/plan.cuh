@@ -8,10 +8,15 @@
 //   plan[P_STATUS]        SERE_* status (kernels after a failed check do nothing)
 //   plan[P_NGROUPS]       number of expert groups (active routed experts ascending, then shared)
 //   plan[P_TOTAL_ROWS]    rows of the permuted batch (each group padded to 16)
-//   plan[P_UNITS_GU/DN]   work units of the gate/up and down grouped GEMMs
+//   plan[P_UNITS_GU/DN]   work units of the gate/up and down phases of the fused FFN
+//   plan[P_TICKET]        work-unit ticket counter of the fused FFN (zeroed by align)
 //   counts[Et]            cells routed to each bank expert (shared experts: T)
 //   group_expert/row0/rows[Et]   bank expert, first permuted row, valid rows of group g
-//   unit_off_gu/dn[Et+1]  prefix of work units per group
+//   sched[Et]             groups in schedule order: padded rows descending (heaviest
+//                         units first -> longest-processing-time-first balancing)
+//   unit_off_gu/dn[Et+1]  prefix of work units over the schedule order
+//   dep[Et]               gate/up units finished per group (the down units of a group
+//                         wait for all of them); zeroed by align
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -25,11 +30,12 @@ enum PlanIdx : int {
   P_UNITS_GU = 3,
   P_UNITS_DN = 4,
   P_NACTIVE = 5,
+  P_TICKET = 6,
   P_HDR = 16
 };
 
 struct PlanOffsets {
-  int counts, group_expert, group_row0, group_rows, unit_off_gu, unit_off_dn, total;
+  int counts, group_expert, group_row0, group_rows, sched, unit_off_gu, unit_off_dn, dep, total;
 };
 
 __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
@@ -38,9 +44,11 @@ __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
   o.group_expert = o.counts + Et;
   o.group_row0 = o.group_expert + Et;
   o.group_rows = o.group_row0 + Et;
-  o.unit_off_gu = o.group_rows + Et;
+  o.sched = o.group_rows + Et;
+  o.unit_off_gu = o.sched + Et;
   o.unit_off_dn = o.unit_off_gu + Et + 1;
-  o.total = o.unit_off_dn + Et + 1;
+  o.dep = o.unit_off_dn + Et + 1;
+  o.total = o.dep + Et;
   return o;
 }
 

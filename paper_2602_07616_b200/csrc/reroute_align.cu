@@ -37,7 +37,7 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   size_t b = 0;
   b += static_cast<size_t>(TK) * 4;                   // s_ids
   b += static_cast<size_t>(M) * 4 * 2;                // s_map, s_list
-  b += static_cast<size_t>(Et) * 4 * 2;               // s_cnt, s_row0
+  b += static_cast<size_t>(Et) * 4 * 4;               // s_cnt, s_row0, s_gpad, s_sched
   b += static_cast<size_t>(kAlignWarps) * Et * 4;     // s_bm (per-warp token masks)
   b += static_cast<size_t>(round_up(TK, 2)) * 2;      // s_rk
   b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb
@@ -65,7 +65,9 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   int32_t* s_list = s_map + M;   // compact list of needed secondaries
   int32_t* s_cnt = s_list + M;   // per bank-expert totals
   int32_t* s_row0 = s_cnt + Et;  // first permuted row of each bank expert's group
-  uint32_t* s_bm = reinterpret_cast<uint32_t*>(s_row0 + Et);          // [warps][Et]
+  int32_t* s_gpad = s_row0 + Et;  // padded rows of group g
+  int32_t* s_sched = s_gpad + Et; // schedule order of the groups
+  uint32_t* s_bm = reinterpret_cast<uint32_t*>(s_sched + Et);         // [warps][Et]
   uint16_t* s_rk = reinterpret_cast<uint16_t*>(s_bm + kAlignWarps * Et);  // [TK] rank inside token block
   uint16_t* s_cntb = s_rk + round_up(TK, 2);                             // [TB][Et] counts -> prefixes
   uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
@@ -315,11 +317,12 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   // group layout: groups = bank experts with cells (ascending) then shared experts; each
   // padded to 16 rows. One warp per chunk of 32 experts scans in parallel, then every
   // chunk adds the totals of the chunks before it.
-  __shared__ int s_tot[4][40];
+  __shared__ int s_tot[2][40];
+  __shared__ int s_ngroups;
   const int nch = (Et + 31) / 32;
   {
     const int e = warp * 32 + lane;
-    int cnt = 0, pad = 0, ugu = 0, udn = 0, gi = 0, r_in = 0, gu_in = 0, dn_in = 0;
+    int cnt = 0, pad = 0, gi = 0, r_in = 0;
     bool act = false;
     if (warp < nch) {
       cnt = e < Et ? s_cnt[e] : 0;
@@ -327,48 +330,77 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       const unsigned m = __ballot_sync(0xffffffffu, act);
       gi = __popc(m & ((1u << lane) - 1u));
       pad = round_up(cnt, kRowAlign);
-      const int ncb = (pad + kColBlock - 1) / kColBlock;
-      ugu = p.tiles_gu * ncb;
-      udn = p.units_dn_per * ncb;
       r_in = warp_incl_scan(pad);
-      gu_in = warp_incl_scan(ugu);
-      dn_in = warp_incl_scan(udn);
       if (lane == 31) {
         s_tot[0][warp] = __popc(m);
         s_tot[1][warp] = r_in;
-        s_tot[2][warp] = gu_in;
-        s_tot[3][warp] = dn_in;
       }
     }
     __syncthreads();
     if (warp < nch) {
-      int gb = 0, rb = 0, gub = 0, dnb = 0;
-      for (int w = 0; w < warp; ++w) { gb += s_tot[0][w]; rb += s_tot[1][w]; gub += s_tot[2][w]; dnb += s_tot[3][w]; }
+      int gb = 0, rb = 0;
+      for (int w = 0; w < warp; ++w) { gb += s_tot[0][w]; rb += s_tot[1][w]; }
       if (e < Et) {
         if (act) {
           plan[po.group_expert + gb + gi] = e;
           plan[po.group_row0 + gb + gi] = rb + r_in - pad;
           plan[po.group_rows + gb + gi] = cnt;
-          plan[po.unit_off_gu + gb + gi] = gub + gu_in - ugu;
-          plan[po.unit_off_dn + gb + gi] = dnb + dn_in - udn;
+          s_gpad[gb + gi] = pad;
         }
         s_row0[e] = act ? rb + r_in - pad : -1;
         plan[po.counts + e] = cnt;
       }
       if (warp == nch - 1 && lane == 0) {
         const int g_tot = gb + s_tot[0][warp], r_tot = rb + s_tot[1][warp];
-        const int gu_tot = gub + s_tot[2][warp], dn_tot = dnb + s_tot[3][warp];
+        s_ngroups = g_tot;
         plan[P_NGROUPS] = g_tot;
         plan[P_TOTAL_ROWS] = r_tot;
-        plan[P_UNITS_GU] = gu_tot;
-        plan[P_UNITS_DN] = dn_tot;
-        plan[po.unit_off_gu + g_tot] = gu_tot;
-        plan[po.unit_off_dn + g_tot] = dn_tot;
+        plan[P_TICKET] = 0;
         if (!reroute) plan[P_NACTIVE] = g_tot - p.n_shared;
       }
     }
   }
   __syncthreads();
+  // schedule order of the fused FFN: padded rows descending, ties by group index (a
+  // unit's cost grows with its column count, so this is longest-processing-time first)
+  const int G = s_ngroups;
+  for (int g = tid; g < G; g += nthr) {
+    const int key = s_gpad[g];
+    int rank = 0;
+    for (int j = 0; j < G; ++j) {
+      const int kj = s_gpad[j];
+      rank += (kj > key) | ((kj == key) & (j < g));
+    }
+    s_sched[rank] = g;
+    plan[po.sched + rank] = g;
+    plan[po.dep + g] = 0;
+  }
+  __syncthreads();
+  if (warp == 0) {  // unit prefixes over the schedule order
+    int gu_base = 0, dn_base = 0;
+    for (int c0 = 0; c0 < G; c0 += 32) {
+      const int i = c0 + lane;
+      int ugu = 0, udn = 0;
+      if (i < G) {
+        const int ncb = (s_gpad[s_sched[i]] + kColBlock - 1) / kColBlock;
+        ugu = p.tiles_gu * ncb;
+        udn = p.units_dn_per * ncb;
+      }
+      const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
+      if (i < G) {
+        plan[po.unit_off_gu + i] = gu_base + gu_in - ugu;
+        plan[po.unit_off_dn + i] = dn_base + dn_in - udn;
+      }
+      gu_base += __shfl_sync(0xffffffffu, gu_in, 31);
+      dn_base += __shfl_sync(0xffffffffu, dn_in, 31);
+    }
+    if (lane == 0) {
+      plan[P_UNITS_GU] = gu_base;
+      plan[P_UNITS_DN] = dn_base;
+      plan[po.unit_off_gu + G] = gu_base;
+      plan[po.unit_off_dn + G] = dn_base;
+    }
+  }
   SERE_PHASE(8);
 
   // ---- pass 2: permuted row of every (token, slot) cell and its inverse

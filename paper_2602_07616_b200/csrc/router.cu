@@ -279,33 +279,44 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
 }
 
 // ------------------------------------------------------------ residual + RMSNorm
-// x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token, fixed-order tree reduction
+// x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token. The traversal
+// (4-element chunks per thread, same block size) and the reduction tree are exactly those
+// of the combine kernel's fused epilogue (layout.cu), so the unfused expert-parallel step
+// reproduces the fused single-GPU step bit for bit.
 __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
                                                                __nv_bfloat16* __restrict__ h, int d_h, float eps) {
   __shared__ float s_red[8];
   const int t = blockIdx.x;
-  float* xr = x + static_cast<size_t>(t) * d_h;
-  const float* yr = y ? y + static_cast<size_t>(t) * d_h : nullptr;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d_h; i += blockDim.x) {
-    float v = xr[i];
-    if (yr) { v += yr[i]; xr[i] = v; }
-    ss = fmaf(v, v, ss);
+  for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
+    const size_t o = static_cast<size_t>(t) * d_h + f0;
+    for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+      float v = x[o + q];
+      if (y) {
+        v = v + y[o + q];
+        x[o + q] = v;
+      }
+      ss = fmaf(v, v, ss);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
-  for (int w = 0; w < (blockDim.x + 31) / 32; ++w) tot += s_red[w];
+  for (int i = 0; i < (blockDim.x + 31) / 32; ++i) tot += s_red[i];
   const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
-  for (int i = threadIdx.x; i < d_h; i += blockDim.x)
-    h[static_cast<size_t>(t) * d_h + i] = __float2bfloat16_rn(xr[i] * r);
+  for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
+    const size_t o = static_cast<size_t>(t) * d_h + f0;
+    for (int q = 0; q < 4 && f0 + q < d_h; ++q) h[o + q] = __float2bfloat16_rn(x[o + q] * r);
+  }
 }
 
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
                                     cudaStream_t stream) {
-  residual_rmsnorm_kernel<<<T, 256, 0, stream>>>(x, y, h_out, d_h, eps);
+  int threads = d_h / 4 >= 256 ? 256 : ((d_h / 4 + 31) / 32) * 32;  // == launch_combine
+  if (threads < 32) threads = 32;
+  residual_rmsnorm_kernel<<<T, threads, 0, stream>>>(x, y, h_out, d_h, eps);
   return cudaGetLastError();
 }
 

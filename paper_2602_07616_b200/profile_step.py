@@ -2,7 +2,7 @@
 
     ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
         --csv --log-file gpurun_out/launches.csv python -m paper_2602_07616_b200.profile_step
-    ncu --profile-from-start off --set full --import-source on -k regex:grouped_gemm -c 2 \
+    ncu --profile-from-start off --set full --import-source on -k regex:moe_ffn -c 2 \
         -o gpurun_out/prof python -m paper_2602_07616_b200.profile_step --layers 2
 
 Only the profiled steps are inside the profiler range (weight generation, packing and
