@@ -87,6 +87,23 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of moe_ffn_kernel from the committed
+    `ncu --set full` capture (newest profiles/r*_ncu_traffic.json), per launch."""
+    files = sorted(ROOT.glob("profiles/r*_ncu_traffic.json"))
+    if not files:
+        return None, None
+    try:
+        d = json.loads(files[-1].read_text())
+        ls = d["launches"]
+        traffic = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in ls) / len(ls)
+        algo = sum(x["algorithmic_bytes"] for x in ls) / len(ls)
+        return traffic, {"file": files[-1].name, "algorithmic_bytes_same_launches": algo,
+                         "traffic_over_algorithmic": round(traffic / algo, 4)}
+    except Exception:
+        return None, None
+
+
 def host_info():
     import platform
 
@@ -363,8 +380,9 @@ def run_ours(args, wl):
         bytes_layers = np.array([algorithmic_bytes(wl_local, a, T) for a in acts_local], dtype=float)
         achieved = float(bytes_layers.sum() / (ffn_ms.sum() * 1e-3) / 1e9)
         peak, peak_kind = measured_peak_hbm()
+        traffic, traffic_src = ncu_traffic()
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "moe_ffn_kernel (gate/up + down phases in one persistent tcgen05 launch)",
                 "peak_kind": peak_kind,
                 "bytes_per_layer_avg": float(bytes_layers.mean()),
