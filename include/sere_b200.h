@@ -199,6 +199,17 @@ int sere_set_stage_events(void* const* events, int n);
  * barrier-separated phases into dev_buf[0..15] (device int64). NULL disables. */
 int sere_debug_set_align_clocks(int64_t* dev_buf);
 
+/* Debug: when non-NULL, the fused FFN kernel writes a per-CTA timeline (globaltimer ns)
+ * into dev_buf[cta * 1024 .. +1024] (device uint64, >= num_SMs * 1024 entries):
+ * [0] start, [1] producer slot-wait, [2] MMA operand-wait, [3] units, [4] producer
+ * dependency-wait, [5] MMA accumulator-wait, [6] epilogue wait, [7] end,
+ * [8+4i] unit i: ticket, t_ticket, t_first_copy, t_last_copy; [816+i] unit i epilogue done.
+ * NULL disables. */
+int sere_debug_set_ffn_trace(uint64_t* dev_buf);
+/* Debug experiments on the fused FFN (outputs become INVALID): bit0 = skip the weight
+ * copies, bit1 = skip the MMAs. 0 = normal operation. */
+int sere_debug_set_ffn_mode(int mode);
+
 /* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).
  * ------------------------------------------------------------------------ */

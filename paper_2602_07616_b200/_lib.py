@@ -69,6 +69,8 @@ SIGNATURES = {
     "sere_residual_rmsnorm": (_c_int, [_p, _p, _p, _c_int, _c_int, ctypes.c_float, _p]),
     "sere_set_stage_events": (_c_int, [ctypes.POINTER(ctypes.c_void_p), _c_int]),
     "sere_debug_set_align_clocks": (_c_int, [_p]),
+    "sere_debug_set_ffn_trace": (_c_int, [_p]),
+    "sere_debug_set_ffn_mode": (_c_int, [_c_int]),
     "sere_layer_workspace_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                              ctypes.POINTER(WsLayout)]),
 }

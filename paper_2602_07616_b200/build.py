@@ -49,6 +49,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     ]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("SERE_NVCC_FLAGS", "").split()  # experiments only (e.g. -DSERE_MW_GU_MAX=1)
     cmd += [str(CSRC / s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

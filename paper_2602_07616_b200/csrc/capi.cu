@@ -35,6 +35,8 @@ int num_sms() {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 long long* g_align_dbg = nullptr;  // sere_debug_set_align_clocks
+unsigned long long* g_ffn_trace = nullptr;  // sere_debug_set_ffn_trace
+int g_ffn_dbg_mode = 0;                     // sere_debug_set_ffn_mode
 
 constexpr int kStageEvents = 6;
 thread_local cudaEvent_t t_stage_events[kStageEvents];
@@ -142,7 +144,8 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.slot_row = slot_row;
   ap.row_token = row_token;
   ap.tiles_gu = d.tiles_gu;
-  ap.units_dn_per = d.tiles_dn * d.ksplit_dn;
+  ap.tiles_dn = d.tiles_dn;
+  ap.ksplit_dn = d.ksplit_dn;
   ap.e_lo = e_lo;
   ap.m_local = m_local;
   ap.dbg = g_align_dbg;
@@ -171,6 +174,8 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   fp.plan = plan;
   fp.Et = L.Et;
   fp.act = activation;
+  fp.trace = g_ffn_trace;
+  fp.dbg_mode = g_ffn_dbg_mode;
   stage_mark(2, stream);
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -401,6 +406,16 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
 
 int sere_debug_set_align_clocks(int64_t* dev_buf) {
   g_align_dbg = reinterpret_cast<long long*>(dev_buf);
+  return SERE_OK;
+}
+
+int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
+  g_ffn_trace = reinterpret_cast<unsigned long long*>(dev_buf);
+  return SERE_OK;
+}
+
+int sere_debug_set_ffn_mode(int mode) {
+  g_ffn_dbg_mode = mode;
   return SERE_OK;
 }
 

@@ -2,34 +2,41 @@
 // the 5th-gen tensor cores (tcgen05), gate/up and down phases fused.
 //
 // Decode-time MoE is expert-weight streaming: each active expert's weights are read
-// once per layer while only 8..256 tokens use them, so the kernel is built to keep
-// HBM busy, not the tensor pipe:
-//  * swap-AB: A = a 128-row weight tile (MMA M = 128 output features), B = the
-//    group's token rows (MMA N = 16..256), D = fp32 accumulator in TMEM;
-//  * weights live in the bank as contiguous 16 KB pre-swizzled tiles, so one bulk
-//    async copy (TMA engine, cp.async.bulk) per k-step streams 16 KB at full DRAM
-//    burst length with an evict-first L2 policy; activations come from the grouped
-//    swizzled buffers (L2-resident, evict-last);
-//  * persistent CTAs (one per SM) take work units from a global ticket counter:
-//    first every gate/up unit (expert group, 64-feature m-tile, column block), then
-//    every down unit (group, 128-feature m-tile, k-split, column block), groups in
-//    the plan's schedule order (padded rows descending = longest-processing-time
-//    first, since a unit's cost grows with its column count). A down unit waits,
-//    before its first copy, until every gate/up unit of its group has published h
-//    (per-group counters in the plan, release/acquire + async-proxy fences), so the
-//    down phase of the heavy groups overlaps the gate/up tail of the light ones and
-//    there is no grid-wide barrier and no second launch;
-//  * the smem ring (6 x 32 KB slots) runs across unit boundaries so the stream
-//    never drains; two TMEM accumulators (2 x 256 columns) let the epilogue of
-//    unit i overlap the MMAs of unit i+1; unit ids reach the MMA and epilogue warps
-//    through a 4-entry smem queue;
-//  * warp roles: warp 0 = producer (one lane), warp 1 = MMA issuer (one lane,
-//    also owns TMEM alloc), warps 2..5 = epilogue (TMEM lane quadrants 2,3,0,1).
+// once per layer while only 8..256 tokens use them. Two bandwidths bound the kernel:
+// HBM (the weights) and the L2 -> SM path, which carries the weights AND every
+// re-read of the activation operand. The design therefore (a) streams weights as
+// large contiguous bulk copies with an evict-first policy and (b) loads each
+// activation tile once per k-step for several weight tiles:
+//  * swap-AB: A = 128-row weight tiles (MMA M = 128 output features), B = the group's
+//    token rows (MMA N = 16..256), D = fp32 accumulators in TMEM;
+//  * a work unit is (phase, expert group, `mw` consecutive m-tiles, column block[, k
+//    split]) -- plan.cuh unit_mw(): a gate/up unit takes 128-feature blocks (a gate
+//    and an up tile each), a down unit up to 2 m-tiles, bounded by the 512 TMEM
+//    columns. One k-step = one B tile + the unit's A tiles, so activations are re-read
+//    d_m/128 (gate/up) and d_h/256 (down) times;
+//  * weights live in the bank as contiguous 16 KB pre-swizzled tiles (one bulk async
+//    copy each, TMA engine); activations come from the grouped swizzled buffers
+//    (L2-resident, evict-last);
+//  * shared memory is a FIFO ring of 13 x 16 KB pages; a k-step takes mw + 1..2
+//    consecutive pages and one (full, empty) mbarrier pair from an 8-entry ring, so the
+//    stream never drains across unit boundaries and needs one commit per k-step;
+//  * TMEM is a ring of columns: a unit takes mw * n_mma columns, the MMA of the next
+//    unit starts as soon as no in-flight unit (4 unit slots, released in order by the
+//    epilogue) holds its columns, so epilogues overlap MMAs whenever two units fit;
+//  * persistent CTAs (one per SM) take units from a global ticket counter: every
+//    gate/up unit first, then every down unit, groups in the plan's schedule order
+//    (padded rows descending). A down unit waits, before its first copy, until every
+//    gate/up unit of its group has published h (per-group counters in the plan,
+//    release/acquire + async-proxy fences): no grid barrier, no second launch;
+//  * warp roles: warp 0 = producer (one lane), warp 1 = MMA issuer (one lane, also owns
+//    the TMEM allocation), warps 2..5 = epilogue (TMEM lane quadrants 2,3,0,1). Page,
+//    column and slot positions are pure functions of the unit sequence, so the three
+//    roles recompute them instead of exchanging them.
 // Epilogues:
-//  * gate/up: A rows interleave gate and up features in 16-row blocks
-//    (pack_w13_kernel), so one warp's TMEM quadrant holds gate (lanes 0-15) and up
-//    (lanes 16-31) of the same 16 features; h = act(g) * u via one shfl_xor, rounded
-//    to bf16, stored straight into the swizzled B layout of the down phase
+//  * gate/up: a feature block's gate tile and up tile (adjacent in the bank, one 32 KB
+//    copy) accumulate into two TMEM accumulators, so the thread owning TMEM lane f
+//    holds gate and up of feature f: h = act(g) * u without any exchange, rounded to
+//    bf16 and stored straight into the swizzled B layout of the down phase
 //    (moe.py:243-245);
 //  * down: fp32 expert outputs per (row, feature), coalesced.
 #include <cuda_bf16.h>
@@ -41,31 +48,35 @@
 
 namespace sere {
 
-constexpr int kSlots = 6;
-constexpr int kSlotBytes = 32768;
+constexpr int kPages = 13;
+constexpr int kPageBytes = 16384;
+constexpr int kEntries = 8;   // k-step barrier ring
+constexpr int kQueue = 4;     // unit-id queue producer -> MMA / epilogue
+constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
 constexpr int kFfnThreads = 192;
-constexpr int kTmemCols = 512;
-constexpr int kQueue = 4;
+static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
 struct Unit {
-  int dn, g, expert, mt, ks, row0, n_mma, rows_valid, kt_begin, kt_end, need;
+  int dn, g, expert, mt0, mwu, ks, row0, n_mma, rows_valid, kt_begin, kt_end, need;
 };
 
 struct __align__(16) FfnSmemTail {
-  uint64_t full[kSlots];
-  uint64_t empty[kSlots];
-  uint64_t tmem_full[2];
-  uint64_t tmem_empty[2];
+  uint64_t full[kEntries];
+  uint64_t empty[kEntries];
+  uint64_t tfull[kTq];
+  uint64_t tempty[kTq];
   uint64_t q_full[kQueue];
   uint64_t q_empty[kQueue];
   int32_t queue[kQueue];
+  int32_t e_page[kEntries], e_np[kEntries];  // producer: pages held by in-flight k-steps
+  int32_t t_col[kTq], t_need[kTq];           // MMA: TMEM columns held by in-flight units
   uint32_t tmem_base;
   int32_t n_groups, units_gu, units_dn;
 };
 
 // per-schedule-position copies of the plan (6 arrays of Et + 1)
 __host__ __device__ inline size_t ffn_smem_bytes(int Et) {
-  return 1024 /*align slack*/ + static_cast<size_t>(kSlots) * kSlotBytes + sizeof(FfnSmemTail) +
+  return 1024 /*align slack*/ + static_cast<size_t>(kPages) * kPageBytes + sizeof(FfnSmemTail) +
          static_cast<size_t>(6) * (Et + 1) * sizeof(int32_t);
 }
 
@@ -87,13 +98,16 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
   const int local = u - uoff[lo];
   const int rows = v.grows[lo];
   const int n16 = round_up(rows, kRowAlign);
-  const int ncb = (n16 + kColBlock - 1) / kColBlock;
+  const int ncb = col_blocks(n16);
+  const int tiles = U.dn ? p.tiles_dn : p.tiles_gu;
+  const int mw = unit_mw(n16, U.dn ? dn_cap(n16) : kMwGuMax, tiles, U.dn ? 1 : 2);
   const int nc = local % ncb;
   const int tmp = local / ncb;
   const int ksplit = U.dn ? p.ksplit_dn : 1;
   const int ktiles = U.dn ? p.ktiles_dn : p.ktiles_gu;
   U.ks = tmp % ksplit;
-  U.mt = tmp / ksplit;
+  U.mt0 = (tmp / ksplit) * mw;
+  U.mwu = min(mw, tiles - U.mt0);
   U.g = v.gid[lo];
   U.expert = v.gexp[lo];
   const int col0 = nc * kColBlock;
@@ -103,21 +117,30 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
   const int kchunk = (ktiles + ksplit - 1) / ksplit;
   U.kt_begin = U.ks * kchunk;
   U.kt_end = min(ktiles, U.kt_begin + kchunk);
-  U.need = p.tiles_gu * ncb;  // gate/up units of this group (the down units' dependency)
+  U.need = group_units_gu(n16, p.tiles_gu);  // gate/up units of this group (the down units' dependency)
   return U;
 }
 
+// A tiles of one k-step: a gate and an up tile per gate/up feature block, one per down m-tile
+__device__ __forceinline__ int kstep_atiles(const Unit& U) { return U.dn ? U.mwu : 2 * U.mwu; }
+// pages of one k-step: the B tile (1 page up to 128 rows, 2 up to 256) then the A tiles
+__device__ __forceinline__ int kstep_pages(const Unit& U) { return (U.n_mma > 128 ? 2 : 1) + kstep_atiles(U); }
+
+__device__ __forceinline__ bool ranges_overlap(int a, int na, int b, int nb) { return a < b + nb && b < a + na; }
+
 __device__ __forceinline__ float act_apply(float g, int act) {
-  if (act == 0) return g * __frcp_rn(1.0f + __expf(-g));  // SiLU (moe.py:28-35)
+  if (act == 0) return __fdividef(g, 1.0f + __expf(-g));  // SiLU (moe.py:28-35); -> -0 for g << 0
   if (act == 1) return fmaxf(g, 0.0f);                     // ReLU (moe.py:38-39)
   const float c = 0.7978845608028654f;                     // GELU-tanh (moe.py:42-45)
   return 0.5f * g * (1.0f + tanhf(c * (g + 0.044715f * g * g * g)));
 }
 
 __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kSlots * kSlotBytes);
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // 1 KB alignment (SW128 atoms) by offsetting the __shared__ array itself, so the
+  // compiler keeps shared-state accesses in the shared address space (LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kPages * kPageBytes);
   int32_t* s_arr = reinterpret_cast<int32_t*>(tail + 1);
   const int E1 = p.Et + 1;
   SchedView sv{s_arr, s_arr + E1, s_arr + 2 * E1, s_arr + 3 * E1, s_arr + 4 * E1, s_arr + 5 * E1};
@@ -129,8 +152,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   const int ng = status == 0 ? plan[P_NGROUPS] : 0;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < kSlots; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tail->tmem_full[i], 1); mbar_init(&tail->tmem_empty[i], 4); }
+    for (int i = 0; i < kEntries; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], 1); }
+    for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], 1); mbar_init(&tail->tempty[i], 4); }
     for (int i = 0; i < kQueue; ++i) { mbar_init(&tail->q_full[i], 1); mbar_init(&tail->q_empty[i], 1 + 4); }
     fence_mbar_init();
     tail->n_groups = ng;
@@ -156,170 +179,220 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   const int n_groups = tail->n_groups, units_gu = tail->units_gu;
   const int units_total = units_gu + tail->units_dn;
   int32_t* dep = plan + po.dep;
+  unsigned long long* tr = p.trace ? p.trace + static_cast<size_t>(blockIdx.x) * kFfnTraceStride : nullptr;
+  if (tr && threadIdx.x == 0) { tr[0] = globaltimer_ns(); tr[813] = clock64(); }
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===================== producer: tickets -> unit queue; bulk async copies into the slot ring
+      // ===================== producer: tickets -> unit queue; bulk async copies into the page ring
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      int slot = 0, qs = 0;
-      uint32_t phase = 0, qph = 0;
-      for (;;) {
+      int qs = 0, nu = 0, head = 0, kstep = 0, oldest = 0;
+      uint32_t qph = 0;
+      unsigned long long w_empty = 0, w_dep = 0, w_q = 0;
+      unsigned long long* acc_empty = tr ? &w_empty : nullptr;
+      for (;; ++nu) {
         const int u = units_total > 0 ? atomicAdd(plan + P_TICKET, 1) : 0;
+        unsigned long long* ut = (tr && nu < kFfnTraceUnits) ? tr + 8 + 4 * nu : nullptr;
+        if (ut) { ut[0] = u; ut[1] = globaltimer_ns(); }
         const bool done = u >= units_total;
-        mbar_wait(&tail->q_empty[qs], qph ^ 1u);
+        mbar_wait_timed(&tail->q_empty[qs], qph ^ 1u, tr ? &w_q : nullptr);
         tail->queue[qs] = done ? -1 : u;
         mbar_arrive(&tail->q_full[qs]);
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
-        if (done) break;
+        if (done) {
+          if (tr) { tr[1] = w_empty; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; }
+          break;
+        }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
         const uint8_t* a_unit;
         const uint8_t* b_base;
+        size_t a_mt_stride;  // bytes between consecutive m-tiles (feature blocks) of the expert
+        uint32_t a_copy;     // bytes of one m-tile at one k-step (gate+up adjacent for gate/up)
         if (U.dn) {
           // h of this group must be complete: every gate/up unit of the group published it
           if (ld_acquire_gpu(dep + U.g) < U.need) {
+            const long long t0 = tr ? clock64() : 0;
             while (ld_acquire_gpu(dep + U.g) < U.need) __nanosleep(64);
+            if (tr) w_dep += static_cast<unsigned long long>(clock64() - t0);
           }
           fence_proxy_async_global();
-          a_unit = p.w2 + (static_cast<size_t>(U.expert) * p.tiles_dn + U.mt) * p.ktiles_dn *
-                              static_cast<size_t>(kTileBytes);
+          a_copy = kTileBytes;
+          a_mt_stride = static_cast<size_t>(p.ktiles_dn) * a_copy;
+          a_unit = p.w2 + (static_cast<size_t>(U.expert) * p.tiles_dn + U.mt0) * a_mt_stride;
           b_base = p.h_pack;
         } else {
-          a_unit = p.w13 + (static_cast<size_t>(U.expert) * p.tiles_gu + U.mt) * p.ktiles_gu *
-                               static_cast<size_t>(kTileBytes);
+          a_copy = 2 * kTileBytes;
+          a_mt_stride = static_cast<size_t>(p.ktiles_gu) * a_copy;
+          a_unit = p.w13 + (static_cast<size_t>(U.expert) * p.tiles_gu + U.mt0) * a_mt_stride;
           b_base = p.x_pack;
         }
-        const int n0 = min(U.n_mma, 128), n1 = U.n_mma - n0;
-        for (int kt = U.kt_begin; kt < U.kt_end; ++kt) {
-          const uint8_t* b_src = b_base + (static_cast<size_t>(kt) * p.r_max + U.row0) * 128;
-          mbar_wait(&tail->empty[slot], phase ^ 1u);
-          uint8_t* sdst = smem + slot * kSlotBytes;
-          mbar_arrive_expect_tx(&tail->full[slot], kTileBytes + n0 * 128);
-          bulk_g2s(sdst, a_unit + static_cast<size_t>(kt) * kTileBytes, kTileBytes, &tail->full[slot], pol_w);
-          bulk_g2s(sdst + kTileBytes, b_src, n0 * 128, &tail->full[slot], pol_x);
-          if (++slot == kSlots) { slot = 0; phase ^= 1u; }
-          if (n1 > 0) {
-            mbar_wait(&tail->empty[slot], phase ^ 1u);
-            sdst = smem + slot * kSlotBytes;
-            mbar_arrive_expect_tx(&tail->full[slot], n1 * 128);
-            bulk_g2s(sdst, b_src + 128 * 128, n1 * 128, &tail->full[slot], pol_x);
-            if (++slot == kSlots) { slot = 0; phase ^= 1u; }
+        if (ut) ut[2] = globaltimer_ns();
+        const int np = kstep_pages(U), bp = np - kstep_atiles(U);
+        const uint32_t b_bytes = static_cast<uint32_t>(U.n_mma) * 128u;
+        const uint32_t tx = b_bytes + ((p.dbg_mode & 1) ? 0u : static_cast<uint32_t>(U.mwu) * a_copy);
+        for (int kt = U.kt_begin; kt < U.kt_end; ++kt, ++kstep) {
+          if (head + np > kPages) head = 0;
+          // release in FIFO order until this k-step's entry and pages are free of every
+          // in-flight k-step (after a wrap the overlap can be with the youngest ones)
+          for (;;) {
+            bool busy = kstep - oldest >= kEntries;
+            for (int s2 = oldest; !busy && s2 < kstep; ++s2)
+              busy = ranges_overlap(head, np, tail->e_page[s2 % kEntries], tail->e_np[s2 % kEntries]);
+            if (!busy) break;
+            mbar_wait_timed(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u,
+                            acc_empty);
+            ++oldest;
           }
+          const int e = kstep % kEntries;
+          tail->e_page[e] = head;
+          tail->e_np[e] = np;
+          uint8_t* pg = smem + head * kPageBytes;
+          mbar_arrive_expect_tx(&tail->full[e], tx);
+          bulk_g2s(pg, b_base + (static_cast<size_t>(kt) * p.r_max + U.row0) * 128, b_bytes, &tail->full[e], pol_x);
+          if (!(p.dbg_mode & 1)) {
+            const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
+            for (int j = 0; j < U.mwu; ++j)
+              bulk_g2s(pg + bp * kPageBytes + j * a_copy, a_kt + j * a_mt_stride, a_copy, &tail->full[e], pol_w);
+          }
+          head += np;
         }
+        if (ut) ut[3] = globaltimer_ns();
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ===================== MMA issuer (single thread)
-      int slot = 0, qs = 0, iter = 0;
-      uint32_t phase = 0, qph = 0;
+      int qs = 0, iter = 0, head = 0, kstep = 0, tcol = 0, oldest = 0;
+      uint32_t qph = 0;
+      unsigned long long w_full = 0, w_tmem = 0, nks = 0;
+      unsigned long long* acc_full = tr ? &w_full : nullptr;
       for (;; ++iter) {
         mbar_wait(&tail->q_full[qs], qph);
         const int u = tail->queue[qs];
         mbar_arrive(&tail->q_empty[qs]);
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
-        if (u < 0) break;
+        if (u < 0) {
+          if (tr) { tr[2] = w_full; tr[5] = w_tmem; tr[810] = nks; }
+          break;
+        }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
-        const int buf = iter & 1;
-        const uint32_t use = static_cast<uint32_t>(iter >> 1);
-        mbar_wait(&tail->tmem_empty[buf], (use & 1u) ^ 1u);
+        // TMEM columns of this unit: FIFO ring over the 512 columns
+        const int na = kstep_atiles(U);
+        const int need = na * U.n_mma;
+        if (tcol + need > kTmemCols) tcol = 0;
+        const int col = tcol;
+        tcol += need;
+        for (;;) {  // release in FIFO order until no in-flight unit holds these columns
+          bool busy = iter - oldest >= kTq;
+          for (int i2 = oldest; !busy && i2 < iter; ++i2)
+            busy = ranges_overlap(col, need, tail->t_col[i2 % kTq], tail->t_need[i2 % kTq]);
+          if (!busy) break;
+          mbar_wait_timed(&tail->tempty[oldest % kTq], static_cast<uint32_t>(oldest / kTq) & 1u,
+                          tr ? &w_tmem : nullptr);
+          ++oldest;
+        }
+        tail->t_col[iter % kTq] = col;
+        tail->t_need[iter % kTq] = need;
         tc_fence_after();
-        const uint32_t d0 = tmem_base + buf * 256;
-        const int n0 = min(U.n_mma, 128), n1 = U.n_mma - n0;
-        const uint32_t idesc0 = umma_idesc_bf16(128, n0);
-        const uint32_t idesc1 = n1 > 0 ? umma_idesc_bf16(128, n1) : 0u;
-        for (int kt = U.kt_begin; kt < U.kt_end; ++kt) {
-          const int s0 = slot;
-          mbar_wait(&tail->full[s0], phase);
-          if (++slot == kSlots) { slot = 0; phase ^= 1u; }
-          int s1 = -1;
-          if (n1 > 0) {
-            s1 = slot;
-            mbar_wait(&tail->full[s1], phase);
-            if (++slot == kSlots) { slot = 0; phase ^= 1u; }
-          }
+        const int np = kstep_pages(U), bp = np - na;
+        const uint32_t idesc = umma_idesc_bf16(128, U.n_mma);
+        const uint32_t d0 = tmem_base + col;
+        for (int kt = U.kt_begin; kt < U.kt_end; ++kt, ++kstep) {
+          if (head + np > kPages) head = 0;
+          const int e = kstep % kEntries;
+          mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u, acc_full);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + s0 * kSlotBytes);
-          const uint32_t b0_addr = a_addr + kTileBytes;
+          const uint32_t b_addr = smem_u32(smem + head * kPageBytes);
+          if (!(p.dbg_mode & 2)) {
+            for (int j = 0; j < na; ++j) {  // A tile j -> accumulator j (gate/up: 2f = gate, 2f+1 = up)
+              const uint32_t a_addr = b_addr + (bp + j) * kPageBytes;
+              const uint32_t dj = d0 + j * U.n_mma;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t acc = (kt > U.kt_begin || k > 0) ? 1u : 0u;
-            umma_bf16(d0, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b0_addr + 32 * k), idesc0, acc);
-          }
-          if (n1 > 0) {
-            const uint32_t b1_addr = smem_u32(smem + s1 * kSlotBytes);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t acc = (kt > U.kt_begin || k > 0) ? 1u : 0u;
-              umma_bf16(d0 + 128, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b1_addr + 32 * k), idesc1,
-                        acc);
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t acc = (kt > U.kt_begin || k > 0) ? 1u : 0u;
+                umma_bf16(dj, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc, acc);
+              }
             }
           }
-          umma_commit(&tail->empty[s0]);
-          if (s1 >= 0) umma_commit(&tail->empty[s1]);
+          ++nks;
+          umma_commit(&tail->empty[e]);
+          head += np;
         }
-        umma_commit(&tail->tmem_full[buf]);
+        umma_commit(&tail->tfull[iter % kTq]);
       }
     }
   } else {
     // ===================== epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
     const int q = warp & 3;
-    int qs = 0, iter = 0;
+    int qs = 0, iter = 0, tcol = 0;
     uint32_t qph = 0;
+    unsigned long long w_tf = 0;
     for (;; ++iter) {
       mbar_wait(&tail->q_full[qs], qph);
       const int u = tail->queue[qs];
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->q_empty[qs]);
       if (++qs == kQueue) { qs = 0; qph ^= 1u; }
-      if (u < 0) break;
+      if (u < 0) {
+        if (tr && warp == 2 && lane == 0) tr[6] = w_tf;
+        break;
+      }
       const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
-      const int buf = iter & 1;
-      const uint32_t use = static_cast<uint32_t>(iter >> 1);
-      mbar_wait(&tail->tmem_full[buf], use & 1u);
+      const int need = kstep_atiles(U) * U.n_mma;
+      if (tcol + need > kTmemCols) tcol = 0;
+      const int col = tcol;
+      tcol += need;
+      mbar_wait_timed(&tail->tfull[iter % kTq], static_cast<uint32_t>(iter / kTq) & 1u,
+                      (tr && warp == 2 && lane == 0) ? &w_tf : nullptr);
+      __syncwarp();
       tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * 256;
+      const uint32_t tq = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col;
       if (!U.dn) {
-        // lanes 0-15: gate of feature f, lanes 16-31: up of the same f
-        const int f = 16 * q + (lane & 15);  // feature within the 64-feature tile == column of h tile
-        const int chunk = f >> 3;
-        uint8_t* hbase = p.h_pack + static_cast<size_t>(U.mt) * p.r_max * 128;
-        for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+        // feature f of block fb: its gate and up accumulators sit in this thread's TMEM lane,
+        // so h = act(g) * u needs no data exchange; one bf16 per (row, f) into the swizzled
+        // B layout of the down phase
+        for (int j = 0; j < U.mwu; ++j) {
+          const int f = (U.mt0 + j) * 128 + q * 32 + lane;
+          const int fl = f & 63;
+          uint8_t* hbase = p.h_pack + static_cast<size_t>(f >> 6) * p.r_max * 128 + (fl & 7) * 2;
+          const uint32_t tg = tq + (2 * j) * U.n_mma, tu = tg + U.n_mma;
+          for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
+            uint32_t rg[16], ru[16];
+            tmem_ld16(tg + c0, rg);
+            tmem_ld16(tu + c0, ru);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float g = __uint_as_float(r[i]);
-            const float up = __shfl_xor_sync(0xffffffffu, g, 16);
-            const float h = act_apply(g, p.act) * up;
-            const float h_next = __shfl_down_sync(0xffffffffu, h, 1);
-            if (lane < 16 && (lane & 1) == 0) {
+            for (int i = 0; i < 16; ++i) {
               const int row = U.row0 + c0 + i;
-              __nv_bfloat162 pair = __floats2bfloat162_rn(h, h_next);
-              uint8_t* dst = hbase + static_cast<size_t>(row) * 128 + sw128_chunk(chunk, row) * 16 + (f & 7) * 2;
-              *reinterpret_cast<__nv_bfloat162*>(dst) = pair;
+              const float h = act_apply(__uint_as_float(rg[i]), p.act) * __uint_as_float(ru[i]);
+              *reinterpret_cast<__nv_bfloat16*>(hbase + static_cast<size_t>(row) * 128 +
+                                                sw128_chunk(fl >> 3, row) * 16) = __float2bfloat16_rn(h);
             }
           }
         }
       } else {
-        const int feat = U.mt * 128 + q * 32 + lane;
-        float* ybase = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * p.d_h_pad;
-        for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+        for (int j = 0; j < U.mwu; ++j) {
+          const int feat = (U.mt0 + j) * 128 + q * 32 + lane;
+          float* ybase = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * p.d_h_pad;
+          const uint32_t taddr = tq + j * U.n_mma;
+          for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(taddr + c0, r);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int j = c0 + i;
-            if (j < U.rows_valid)
-              ybase[static_cast<size_t>(U.row0 + j) * p.d_h_pad + feat] = __uint_as_float(r[i]);
+            for (int i = 0; i < 16; ++i) {
+              const int jr = c0 + i;
+              if (jr < U.rows_valid)
+                ybase[static_cast<size_t>(U.row0 + jr) * p.d_h_pad + feat] = __uint_as_float(r[i]);
+            }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tail->tmem_empty[buf]);
+      if (lane == 0) mbar_arrive(&tail->tempty[iter % kTq]);
+      if (tr && warp == 2 && lane == 0 && iter < kFfnTraceUnits) tr[816 + iter] = globaltimer_ns();
       if (!U.dn) {
         // publish this unit's slice of h: the down units of the group (any SM) read it with
         // bulk copies (async proxy) after acquiring the counter
@@ -336,6 +409,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tr && threadIdx.x == 0) { tr[7] = globaltimer_ns(); tr[814] = clock64(); }
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 

@@ -19,80 +19,17 @@
 namespace sere {
 
 // ------------------------------------------------------------------ packing
-// W13 tile (e, mt, kt): row r of 128 -> block b=r/32, j=r%32: j<16 gate feature
-// 64*mt+16*b+j, else up feature 64*mt+16*b+j-16; column c -> input k = 64*kt + c.
-__global__ void __launch_bounds__(256) pack_w13_kernel(const __nv_bfloat16* __restrict__ wg,
-                                                       const __nv_bfloat16* __restrict__ wu, int d_h, int d_m,
-                                                       int tiles, int ktiles, uint8_t* __restrict__ w13,
-                                                       int first, int unpack) {
-  __shared__ __nv_bfloat16 sg[64][66];
-  __shared__ __nv_bfloat16 su[64][66];
-  const int tile = blockIdx.x;
-  const int kt = tile % ktiles;
-  const int mt = (tile / ktiles) % tiles;
-  const int e = tile / (ktiles * tiles);
-  uint8_t* dst = w13 + (static_cast<size_t>((first + e) * tiles + mt) * ktiles + kt) * kTileBytes;
-  const size_t ebase = static_cast<size_t>(e) * d_h * d_m;
-  if (!unpack) {
-    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-      const int kk = i / 64, ff = i % 64;
-      const int k = kt * 64 + kk, f = mt * 64 + ff;
-      const bool ok = k < d_h && f < d_m;
-      sg[kk][ff] = ok ? wg[ebase + static_cast<size_t>(k) * d_m + f] : __float2bfloat16(0.f);
-      su[kk][ff] = ok ? wu[ebase + static_cast<size_t>(k) * d_m + f] : __float2bfloat16(0.f);
-    }
-    __syncthreads();
-    for (int cid = threadIdx.x; cid < 128 * 8; cid += blockDim.x) {
-      const int r = cid / 8, c = cid % 8;
-      const int j = r % 32;
-      const int ff = 16 * (r / 32) + (j & 15);
-      __nv_bfloat16 (*src)[66] = j < 16 ? sg : su;
-      alignas(16) __nv_bfloat16 v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = src[c * 8 + q][ff];
-      *reinterpret_cast<uint4*>(dst + r * 128 + sw128_chunk(c, r) * 16) = *reinterpret_cast<uint4*>(v);
-    }
-  } else {
-    for (int cid = threadIdx.x; cid < 128 * 8; cid += blockDim.x) {
-      const int r = cid / 8, c = cid % 8;
-      const int j = r % 32;
-      const int ff = 16 * (r / 32) + (j & 15);
-      __nv_bfloat16 (*tgt)[66] = j < 16 ? sg : su;
-      alignas(16) __nv_bfloat16 v[8];
-      *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(dst + r * 128 + sw128_chunk(c, r) * 16);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) tgt[c * 8 + q][ff] = v[q];
-    }
-    __syncthreads();
-    __nv_bfloat16* og = const_cast<__nv_bfloat16*>(wg);
-    __nv_bfloat16* ou = const_cast<__nv_bfloat16*>(wu);
-    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-      const int kk = i / 64, ff = i % 64;
-      const int k = kt * 64 + kk, f = mt * 64 + ff;
-      if (k < d_h && f < d_m) {
-        og[ebase + static_cast<size_t>(k) * d_m + f] = sg[kk][ff];
-        ou[ebase + static_cast<size_t>(k) * d_m + f] = su[kk][ff];
-      }
-    }
-  }
-}
-
-// W2 tile (e, mt, kt): row r -> output feature o = 128*mt + r; column c -> k = 64*kt + c (d_m index)
-__global__ void __launch_bounds__(256) pack_w2_kernel(const __nv_bfloat16* __restrict__ wd, int d_h, int d_m,
-                                                      int tiles, int ktiles, uint8_t* __restrict__ w2, int first,
-                                                      int unpack) {
-  __shared__ __nv_bfloat16 sd[64][130];
-  const int tile = blockIdx.x;
-  const int kt = tile % ktiles;
-  const int mt = (tile / ktiles) % tiles;
-  const int e = tile / (ktiles * tiles);
-  uint8_t* dst = w2 + (static_cast<size_t>((first + e) * tiles + mt) * ktiles + kt) * kTileBytes;
-  const size_t ebase = static_cast<size_t>(e) * d_m * d_h;
+// A bank tile is 128 output features x 64 input features of a weight W[K][F] kept in
+// the reference's x @ W orientation (row-major, ExpertWeights moe.py:70-77): tile
+// row r = feature f0 + r, column c = input k0 + c, bf16, 128-B rows with the 16-B
+// chunk swizzle of the UMMA SW128 K-major layout. Out-of-range entries are zero.
+__device__ __forceinline__ void tile_xfer(const __nv_bfloat16* __restrict__ W, int K, int F, int f0, int k0,
+                                          uint8_t* __restrict__ dst, int unpack, __nv_bfloat16 (*sd)[130]) {
   if (!unpack) {
     for (int i = threadIdx.x; i < 64 * 128; i += blockDim.x) {
-      const int kk = i / 128, oo = i % 128;
-      const int k = kt * 64 + kk, o = mt * 128 + oo;
-      sd[kk][oo] = (k < d_m && o < d_h) ? wd[ebase + static_cast<size_t>(k) * d_h + o] : __float2bfloat16(0.f);
+      const int kk = i / 128, ff = i % 128;
+      const int k = k0 + kk, f = f0 + ff;
+      sd[kk][ff] = (k < K && f < F) ? W[static_cast<size_t>(k) * F + f] : __float2bfloat16(0.f);
     }
     __syncthreads();
     for (int cid = threadIdx.x; cid < 128 * 8; cid += blockDim.x) {
@@ -111,13 +48,44 @@ __global__ void __launch_bounds__(256) pack_w2_kernel(const __nv_bfloat16* __res
       for (int q = 0; q < 8; ++q) sd[c * 8 + q][r] = v[q];
     }
     __syncthreads();
-    __nv_bfloat16* od = const_cast<__nv_bfloat16*>(wd);
+    __nv_bfloat16* out = const_cast<__nv_bfloat16*>(W);
     for (int i = threadIdx.x; i < 64 * 128; i += blockDim.x) {
-      const int kk = i / 128, oo = i % 128;
-      const int k = kt * 64 + kk, o = mt * 128 + oo;
-      if (k < d_m && o < d_h) od[ebase + static_cast<size_t>(k) * d_h + o] = sd[kk][oo];
+      const int kk = i / 128, ff = i % 128;
+      const int k = k0 + kk, f = f0 + ff;
+      if (k < K && f < F) out[static_cast<size_t>(k) * F + f] = sd[kk][ff];
     }
   }
+}
+
+// W13 tile (e, fb, kt, s): s = 0 gate / 1 up, features 128*fb.., inputs 64*kt.. of
+// w_gate / w_up [d_h, d_m]; the gate and up tiles of one (fb, kt) are adjacent (one
+// 32 KB copy feeds both accumulators of the SwiGLU epilogue).
+__global__ void __launch_bounds__(256) pack_w13_kernel(const __nv_bfloat16* __restrict__ wg,
+                                                       const __nv_bfloat16* __restrict__ wu, int d_h, int d_m,
+                                                       int tiles, int ktiles, uint8_t* __restrict__ w13,
+                                                       int first, int unpack) {
+  __shared__ __nv_bfloat16 sd[64][130];
+  const int tile = blockIdx.x;
+  const int s = tile & 1;
+  const int kt = (tile >> 1) % ktiles;
+  const int fb = ((tile >> 1) / ktiles) % tiles;
+  const int e = (tile >> 1) / (ktiles * tiles);
+  uint8_t* dst = w13 + ((static_cast<size_t>((first + e) * tiles + fb) * ktiles + kt) * 2 + s) * kTileBytes;
+  const __nv_bfloat16* W = (s ? wu : wg) + static_cast<size_t>(e) * d_h * d_m;
+  tile_xfer(W, d_h, d_m, fb * 128, kt * 64, dst, unpack, sd);
+}
+
+// W2 tile (e, mt, kt): output features 128*mt.., inputs 64*kt.. of w_down [d_m, d_h]
+__global__ void __launch_bounds__(256) pack_w2_kernel(const __nv_bfloat16* __restrict__ wd, int d_h, int d_m,
+                                                      int tiles, int ktiles, uint8_t* __restrict__ w2, int first,
+                                                      int unpack) {
+  __shared__ __nv_bfloat16 sd[64][130];
+  const int tile = blockIdx.x;
+  const int kt = tile % ktiles;
+  const int mt = (tile / ktiles) % tiles;
+  const int e = tile / (ktiles * tiles);
+  uint8_t* dst = w2 + (static_cast<size_t>((first + e) * tiles + mt) * ktiles + kt) * kTileBytes;
+  tile_xfer(wd + static_cast<size_t>(e) * d_m * d_h, d_m, d_h, mt * 128, kt * 64, dst, unpack, sd);
 }
 
 cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const __nv_bfloat16* wd, int count,
@@ -125,7 +93,7 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
   if (count <= 0) return cudaSuccess;
   uint8_t* w13 = bank;
   uint8_t* w2 = bank + bank_w13_bytes(Et, d);
-  const unsigned g13 = static_cast<unsigned>(count) * d.tiles_gu * d.ktiles_gu;
+  const unsigned g13 = static_cast<unsigned>(count) * d.tiles_gu * d.ktiles_gu * 2;
   const unsigned g2 = static_cast<unsigned>(count) * d.tiles_dn * d.ktiles_dn;
   pack_w13_kernel<<<g13, 256, 0, stream>>>(wg, wu, d.d_h, d.d_m, d.tiles_gu, d.ktiles_gu, w13, first, unpack);
   pack_w2_kernel<<<g2, 256, 0, stream>>>(wd, d.d_h, d.d_m, d.tiles_dn, d.ktiles_dn, w2, first, unpack);

@@ -28,8 +28,7 @@ struct AlignParams {
   int32_t* plan;
   int32_t* slot_row;
   int32_t* row_token;
-  int tiles_gu;      // gate/up units per column block
-  int units_dn_per;  // down units per column block (tiles_dn * ksplit_dn)
+  int tiles_gu, tiles_dn, ksplit_dn;  // FFN geometry (work units: plan.cuh group_units_*)
   int e_lo, m_local; // expert-parallel ownership: bank holds global experts [e_lo, e_lo+m_local)
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
 };
@@ -45,7 +44,11 @@ struct FfnParams {
   int32_t* plan;          // written by reroute_align; the ticket and dep counters are updated here
   int Et;
   int act;
+  int dbg_mode;               // debug experiments: bit0 skip weight copies, bit1 skip MMAs (results invalid)
+  unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
 };
+constexpr int kFfnTraceStride = 1024;
+constexpr int kFfnTraceUnits = 200;
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);

@@ -59,9 +59,48 @@ constexpr int kTileBytes = 16384; // 128 rows x 64 bf16
 
 __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
+// ---- work-unit geometry of the fused FFN (shared by the planner and the kernel)
+// A unit covers `mw` consecutive m-tiles of one expert group and one column block of
+// its rows: every k-step loads the block's activation tile (B) ONCE and multiplies it
+// with every weight tile (A) of the unit -- gate AND up for a gate/up feature block --
+// so activations are re-read tiles/mw times. TMEM bounds mw: the unit's accumulators
+// (2 per gate/up block, 1 per down m-tile) of n_mma fp32 columns fit 512 columns.
+constexpr int kTmemCols = 512;
+#ifndef SERE_MW_GU_MAX
+#define SERE_MW_GU_MAX 1
+#endif
+#ifndef SERE_MW_DN_MAX
+#define SERE_MW_DN_MAX 2
+#endif
+constexpr int kMwGuMax = SERE_MW_GU_MAX;  // gate/up: feature blocks of 128 (2 accumulators each)
+constexpr int kMwDnMax = SERE_MW_DN_MAX;  // down: 2 x 128 features (uniform, small units finish the step evenly)
+
+// accs = TMEM accumulators per m-tile (2 for gate/up: gate and up; 1 for down)
+__host__ __device__ inline int unit_mw(int n16, int cap, int tiles, int accs = 1) {
+  const int nb = n16 < kColBlock ? (n16 > 0 ? n16 : kRowAlign) : kColBlock;
+  int mw = kTmemCols / (nb * accs);
+  mw = mw < cap ? mw : cap;
+  mw = mw < tiles ? mw : tiles;
+  return mw < 1 ? 1 : mw;
+}
+__host__ __device__ inline int col_blocks(int n16) { return (n16 + kColBlock - 1) / kColBlock; }
+__host__ __device__ inline int group_units_gu(int n16, int tiles_gu) {
+  const int mw = unit_mw(n16, kMwGuMax, tiles_gu, 2);
+  return col_blocks(n16) * ((tiles_gu + mw - 1) / mw);
+}
+#ifndef SERE_DN_SMALL_N
+#define SERE_DN_SMALL_N 0
+#endif
+// down units of small groups (scheduled last) take one m-tile: they finish the step
+__host__ __device__ inline int dn_cap(int n16) { return n16 <= SERE_DN_SMALL_N ? 1 : kMwDnMax; }
+__host__ __device__ inline int group_units_dn(int n16, int tiles_dn, int ksplit_dn) {
+  const int mw = unit_mw(n16, dn_cap(n16), tiles_dn);
+  return col_blocks(n16) * ((tiles_dn + mw - 1) / mw) * ksplit_dn;
+}
+
 struct Dims {
   int d_h, d_m, d_h_pad, d_m_pad;
-  int tiles_gu;   // gate/up m-tiles per expert: d_m_pad/64 (each 64 features = 128 MMA rows gate|up)
+  int tiles_gu;   // gate/up feature blocks per expert: d_m_pad/128 (a gate tile + an up tile each)
   int ktiles_gu;  // d_h_pad/64
   int tiles_dn;   // down m-tiles per expert: d_h_pad/128
   int ktiles_dn;  // d_m_pad/64
@@ -73,8 +112,8 @@ inline Dims make_dims(int d_h, int d_m) {
   d.d_h = d_h;
   d.d_m = d_m;
   d.d_h_pad = round_up(d_h, 128);
-  d.d_m_pad = round_up(d_m, 64);
-  d.tiles_gu = d.d_m_pad / 64;
+  d.d_m_pad = round_up(d_m, 128);
+  d.tiles_gu = d.d_m_pad / 128;
   d.ktiles_gu = d.d_h_pad / 64;
   d.tiles_dn = d.d_h_pad / 128;
   d.ktiles_dn = d.d_m_pad / 64;
@@ -88,9 +127,9 @@ inline Dims make_dims(int d_h, int d_m) {
   return d;
 }
 
-// bank layout: W13 tiles [Et][tiles_gu][ktiles_gu] then W2 tiles [Et][tiles_dn][ktiles_dn]
+// bank layout: W13 tiles [Et][tiles_gu][ktiles_gu][gate, up] then W2 tiles [Et][tiles_dn][ktiles_dn]
 inline size_t bank_w13_bytes(int Et, const Dims& d) {
-  return static_cast<size_t>(Et) * d.tiles_gu * d.ktiles_gu * kTileBytes;
+  return static_cast<size_t>(Et) * d.tiles_gu * d.ktiles_gu * 2 * kTileBytes;
 }
 inline size_t bank_w2_bytes(int Et, const Dims& d) {
   return static_cast<size_t>(Et) * d.tiles_dn * d.ktiles_dn * kTileBytes;

@@ -382,9 +382,9 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       const int i = c0 + lane;
       int ugu = 0, udn = 0;
       if (i < G) {
-        const int ncb = (s_gpad[s_sched[i]] + kColBlock - 1) / kColBlock;
-        ugu = p.tiles_gu * ncb;
-        udn = p.units_dn_per * ncb;
+        const int n16 = s_gpad[s_sched[i]];
+        ugu = group_units_gu(n16, p.tiles_gu);
+        udn = group_units_dn(n16, p.tiles_dn, p.ksplit_dn);
       }
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {

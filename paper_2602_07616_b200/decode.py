@@ -169,6 +169,7 @@ class DecodeStep(StageEvents):
             self.outs.append(_moe.LayerOutput(y, None, rr.status, rr))
         self.graph = None
         self.stage_events = None
+        self._trace_hook = None  # debug_ffn: called with the layer index before each layer launch
         _moe.workspace(T, model.K, model.M, model.n_shared, model.d_h, model.d_m, dev)
 
     # ---------------------------------------------------------------- launches
@@ -190,6 +191,8 @@ class DecodeStep(StageEvents):
                 else:
                     self.h.copy_(self.outs[l - 1].y)
             _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
+            if self._trace_hook is not None:
+                self._trace_hook(l)
             self._events_on(l)
             if plain:
                 _moe.moe_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
@@ -203,8 +206,9 @@ class DecodeStep(StageEvents):
 
     @property
     def launches_per_step(self) -> int:
-        """Kernels of this library per step: router + 5 layer kernels per layer (+ the first RMSNorm)."""
-        return self.model.L * 6 + (0 if self.block == "plain" else 1)
+        """Kernels of this library per step: router + 4 layer kernels (re-route/align, permute,
+        fused FFN, combine) per layer (+ the first RMSNorm)."""
+        return self.model.L * 5 + (0 if self.block == "plain" else 1)
 
     def run(self) -> None:
         """One step on the current stream (graph replay if captured)."""

@@ -187,7 +187,9 @@ class EPDecodeStep(StageEvents):
 
     @property
     def launches_per_step(self) -> int:
-        return self.model.L * 7 + 1
+        """Kernels of this library per step: router, re-route/align, permute, fused FFN, combine and
+        residual RMSNorm per layer, plus the first RMSNorm (NCCL and torch copies not counted)."""
+        return self.model.L * 6 + 1
 
     def run(self) -> None:
         if self.graph is not None:
