@@ -209,6 +209,8 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf);
 /* Debug experiments on the fused FFN (outputs become INVALID): bit0 = skip the weight
  * copies, bit1 = skip the MMAs. 0 = normal operation. */
 int sere_debug_set_ffn_mode(int mode);
+/* Debug: router phase clocks (clock64) per CTA, dev_buf[cta * 8 + phase]. NULL disables. */
+int sere_debug_set_route_clocks(int64_t* dev_buf);
 
 /* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).

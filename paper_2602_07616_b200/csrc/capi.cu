@@ -414,6 +414,11 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
   return SERE_OK;
 }
 
+int sere_debug_set_route_clocks(int64_t* dev_buf) {
+  g_route_dbg = reinterpret_cast<long long*>(dev_buf);
+  return SERE_OK;
+}
+
 int sere_debug_set_ffn_mode(int mode) {
   g_ffn_dbg_mode = mode;
   return SERE_OK;

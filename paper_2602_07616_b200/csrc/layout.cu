@@ -15,6 +15,7 @@
 #include "params.cuh"
 #include "plan.cuh"
 #include "ptx.cuh"
+#include "rowops.cuh"
 
 namespace sere {
 
@@ -101,7 +102,11 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 }
 
 // ------------------------------------------------------------------ permute
-// x_pack[kt][row][64] (128-B rows, chunk-swizzled) <- x[row_token[row]][64*kt .. +64]
+// x_pack[kt][row][64] (128-B rows, chunk-swizzled) <- x[row_token[row]][64*kt .. +64].
+// One warp per permuted row: the source token is read once, then every lane keeps
+// kPermVec independent 16-B loads in flight before storing (a latency-bound gather).
+constexpr int kPermVec = 8;
+
 __global__ void __launch_bounds__(256) permute_kernel(const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad,
                                                       const int32_t* __restrict__ plan,
                                                       const int32_t* __restrict__ row_token, int r_max,
@@ -109,35 +114,46 @@ __global__ void __launch_bounds__(256) permute_kernel(const __nv_bfloat16* __res
   if (plan[P_STATUS] != 0) return;
   const int total_rows = plan[P_TOTAL_ROWS];
   const int cpr = d_h_pad / 8;  // 16-B chunks per row
-  const long long n = static_cast<long long>(total_rows) * cpr;
+  const int lane = threadIdx.x & 31;
   const bool vec = (d_h & 7) == 0;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / cpr), ch = static_cast<int>(i % cpr);
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < total_rows; r += (gridDim.x * blockDim.x) >> 5) {
     const int t = row_token[r];
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    const int k0 = ch * 8;
-    if (t >= 0 && k0 < d_h) {
-      const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
-      if (vec) {
-        v = *reinterpret_cast<const uint4*>(src);
-      } else {
-        alignas(16) __nv_bfloat16 tmp[8];
+    for (int c0 = 0; c0 < cpr; c0 += 32 * kPermVec) {
+      uint4 v[kPermVec];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) tmp[q] = (k0 + q < d_h) ? src[q] : __float2bfloat16(0.f);
-        v = *reinterpret_cast<uint4*>(tmp);
+      for (int i = 0; i < kPermVec; ++i) {
+        const int ch = c0 + lane + 32 * i;
+        const int k0 = ch * 8;
+        v[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (t >= 0 && ch < cpr && k0 < d_h) {
+          const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
+          if (vec) {
+            v[i] = __ldg(reinterpret_cast<const uint4*>(src));
+          } else {
+            alignas(16) __nv_bfloat16 tmp[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tmp[q] = (k0 + q < d_h) ? src[q] : __float2bfloat16(0.f);
+            v[i] = *reinterpret_cast<uint4*>(tmp);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kPermVec; ++i) {
+        const int ch = c0 + lane + 32 * i;
+        if (ch < cpr) {
+          const int kt = ch >> 3, c = ch & 7;
+          *reinterpret_cast<uint4*>(x_pack + (static_cast<size_t>(kt) * r_max + r) * 128 + sw128_chunk(c, r) * 16) =
+              v[i];
+        }
       }
     }
-    const int kt = ch >> 3, c = ch & 7;
-    *reinterpret_cast<uint4*>(x_pack + (static_cast<size_t>(kt) * r_max + r) * 128 + sw128_chunk(c, r) * 16) = v;
   }
 }
 
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, const int32_t* row_token,
                            int r_max, uint8_t* x_pack, int num_sms, cudaStream_t stream) {
-  const long long work = static_cast<long long>(r_max) * (d.d_h_pad / 8);
-  int blocks = static_cast<int>((work + 255) / 256);
-  blocks = blocks < num_sms * 8 ? blocks : num_sms * 8;
+  int blocks = (r_max + 7) / 8;  // one warp per row, 8 warps per CTA
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (blocks < 1) blocks = 1;
   permute_kernel<<<blocks, 256, 0, stream>>>(x, d.d_h, d.d_h_pad, plan, row_token, r_max, x_pack);
   return cudaGetLastError();
@@ -149,14 +165,20 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 // separately (no FMA contraction), mirroring numpy's `y[rows] += w * E(x)`.
 // Optional decode-block epilogue (x_res != null): x_res[t] += y[t], then
 // h_next[t] = bf16(x_res[t] * rsqrt(mean(x_res[t]^2) + eps)) -- the residual add and the
-// next layer's RMSNorm fused into the same pass over the token row (one CTA per token).
-__device__ __forceinline__ float4 load_y_sum(const float* src, int ksplit, size_t split_stride) {
-  float4 v = *reinterpret_cast<const float4*>(src);
+// next layer's RMSNorm fused into the same pass over the token row.
+// One CTA per token (rowops.cuh traversal); each thread gathers its 8 features of up to
+// kCombBatch slots at once so that many loads are in flight.
+constexpr int kCombBatch = 4;
+
+__device__ __forceinline__ void load_y8(const float* src, int ksplit, size_t split_stride, float (&v)[8]) {
+  float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
   for (int s = 1; s < ksplit; ++s) {
-    const float4 o = *reinterpret_cast<const float4*>(src + s * split_stride);
-    v.x = __fadd_rn(v.x, o.x); v.y = __fadd_rn(v.y, o.y); v.z = __fadd_rn(v.z, o.z); v.w = __fadd_rn(v.w, o.w);
+    const float4 oa = *reinterpret_cast<const float4*>(src + s * split_stride);
+    const float4 ob = *reinterpret_cast<const float4*>(src + s * split_stride + 4);
+    a.x = __fadd_rn(a.x, oa.x); a.y = __fadd_rn(a.y, oa.y); a.z = __fadd_rn(a.z, oa.z); a.w = __fadd_rn(a.w, oa.w);
+    b.x = __fadd_rn(b.x, ob.x); b.y = __fadd_rn(b.y, ob.y); b.z = __fadd_rn(b.z, ob.z); b.w = __fadd_rn(b.w, ob.w);
   }
-  return v;
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 
 __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
@@ -170,57 +192,66 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
   if (plan[P_STATUS] != 0) return;
   const int TK = T * K;
   const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
-  const bool vec = (d_h & 3) == 0;
-  for (int t = blockIdx.x; t < T; t += gridDim.x) {
-    float ss = 0.f;
-    for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int k = 0; k < K; ++k) {
-        const int row = slot_row[t * K + k];
-        if (row < 0) continue;  // expert owned by another rank (expert parallelism)
-        const float wk = w[t * K + k];
-        const float4 v = load_y_sum(y_perm + static_cast<size_t>(row) * d_h_pad + f0, ksplit, split_stride);
-        acc[0] = __fadd_rn(acc[0], __fmul_rn(wk, v.x));
-        acc[1] = __fadd_rn(acc[1], __fmul_rn(wk, v.y));
-        acc[2] = __fadd_rn(acc[2], __fmul_rn(wk, v.z));
-        acc[3] = __fadd_rn(acc[3], __fmul_rn(wk, v.w));
+  const int t = blockIdx.x;
+  float ss = 0.f;
+  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
+    // y_perm rows are d_h_pad (multiple of 128) wide, so the 8-float read never leaves the row
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int k0 = 0; k0 < K + n_shared; k0 += kCombBatch) {
+      int row[kCombBatch];
+      float wk[kCombBatch];
+      float v[kCombBatch][8];
+#pragma unroll
+      for (int b = 0; b < kCombBatch; ++b) {
+        const int k = k0 + b;
+        row[b] = -1;
+        wk[b] = 1.f;
+        if (k < K) {
+          row[b] = slot_row[t * K + k];
+          wk[b] = w[t * K + k];
+        } else if (k < K + n_shared) {
+          row[b] = slot_row[TK + t * n_shared + (k - K)];
+        }
+        if (row[b] >= 0) load_y8(y_perm + static_cast<size_t>(row[b]) * d_h_pad + f0, ksplit, split_stride, v[b]);
       }
-      for (int s = 0; s < n_shared; ++s) {
-        const int row = slot_row[TK + t * n_shared + s];
-        const float4 v = load_y_sum(y_perm + static_cast<size_t>(row) * d_h_pad + f0, ksplit, split_stride);
-        acc[0] = __fadd_rn(acc[0], v.x);
-        acc[1] = __fadd_rn(acc[1], v.y);
-        acc[2] = __fadd_rn(acc[2], v.z);
-        acc[3] = __fadd_rn(acc[3], v.w);
-      }
-      const size_t o = static_cast<size_t>(t) * d_h + f0;
-      if (y) {
-        if (vec) *reinterpret_cast<float4*>(y + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        else for (int q = 0; q < 4 && f0 + q < d_h; ++q) y[o + q] = acc[q];
-      }
-      if (y_bf16)
-        for (int q = 0; q < 4 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[q]);
-      if (x_res) {
-        for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
-          const float v = x_res[o + q] + acc[q];
-          x_res[o + q] = v;
-          ss = fmaf(v, v, ss);
+#pragma unroll
+      for (int b = 0; b < kCombBatch; ++b) {
+        if (row[b] < 0) continue;  // padding of the batch, or an expert owned by another rank (EP)
+        if (k0 + b < K) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wk[b], v[b][q]));
+        } else {  // shared experts: weight 1 (moe.py:308-309)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], v[b][q]);
         }
       }
     }
-    if (x_res) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
-      __syncthreads();
-      float tot = 0.f;
-      for (int i = 0; i < (blockDim.x + 31) / 32; ++i) tot += s_red[i];
-      const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
-      for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
-        const size_t o = static_cast<size_t>(t) * d_h + f0;
-        for (int q = 0; q < 4 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(x_res[o + q] * r);
+    const size_t o = static_cast<size_t>(t) * d_h + f0;
+    const bool full = f0 + 8 <= d_h && (d_h & 3) == 0;
+    if (y) {
+      if (full) {
+        *reinterpret_cast<float4*>(y + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(y + o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      } else {
+        for (int q = 0; q < 8 && f0 + q < d_h; ++q) y[o + q] = acc[q];
       }
-      __syncthreads();
+    }
+    if (y_bf16)
+      for (int q = 0; q < 8 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[q]);
+    if (x_res) {
+      for (int q = 0; q < 8 && f0 + q < d_h; ++q) {
+        const float vv = x_res[o + q] + acc[q];
+        x_res[o + q] = vv;
+        ss = fmaf(vv, vv, ss);
+      }
+    }
+  }
+  if (x_res) {
+    const float tot = block_sum(ss, s_red);
+    const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
+    for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
+      const size_t o = static_cast<size_t>(t) * d_h + f0;
+      for (int q = 0; q < 8 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(x_res[o + q] * r);
     }
   }
 }
@@ -230,10 +261,8 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
                            cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  int threads = d.d_h / 4 >= 256 ? 256 : ((d.d_h / 4 + 31) / 32) * 32;
-  if (threads < 32) threads = 32;
-  combine_kernel<<<T, threads, 0, stream>>>(y_perm, d.ksplit_dn, r_max, d.d_h, d.d_h_pad, plan, slot_row, w, T, K,
-                                            n_shared, y, y_bf16, x_res, h_next, eps);
+  combine_kernel<<<T, row_threads(d.d_h), 0, stream>>>(y_perm, d.ksplit_dn, r_max, d.d_h, d.d_h_pad, plan, slot_row,
+                                                        w, T, K, n_shared, y, y_bf16, x_res, h_next, eps);
   return cudaGetLastError();
 }
 

@@ -50,6 +50,8 @@ struct FfnParams {
 constexpr int kFfnTraceStride = 1024;
 constexpr int kFfnTraceUnits = 200;
 
+extern long long* g_route_dbg;  // router.cu: debug phase clocks of the router (nullptr = off)
+
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);
 cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const __nv_bfloat16* wd, int count,

@@ -11,6 +11,8 @@
 #include <math_constants.h>
 
 #include "params.cuh"
+#include "ptx.cuh"
+#include "rowops.cuh"
 
 namespace sere {
 
@@ -91,15 +93,31 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
   }
 }
 
-// ------------------------------------------------------------------ fast path
-// Tensor-core router for M <= 256, M % 8 == 0, K <= 32: grid (T/32 token tiles, d_h/256
-// K-splits); each CTA stages a 32 x 256 slice of x and the transposed 256 x M slice of
-// W_r in shared memory and issues bf16 mma.sync m16n8k16 (fp32 accumulate): the router
-// GEMM is 0.27 GFLOP/layer and purely latency-bound, so it needs many small CTAs, not
-// TMEM. Partial logits go to the workspace; the LAST CTA of each token tile (atomic
-// ticket) sums the splits in split order (deterministic), adds the bias and runs the
-// warp top-K + softmax, then resets its ticket for the next launch.
-constexpr int kRtTok = 32, kRtKC = 256, kRtPad = 8;
+// Fast path (M % 8 == 0, M <= 256, K <= 32, d_h % 8 == 0): one thread-block CLUSTER per
+// 16-token tile, its S CTAs split d_h into S chunks of kc. Each CTA stages its x rows and
+// W_r^T rows with cp.async (one round trip), runs mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate) into a [16][M] partial in its own shared memory; after a cluster
+// barrier the CTAs exchange row slices of their partials over distributed shared memory
+// (bulk copies), so that each CTA owns 16/S tokens: it sums their S partials in split
+// order (deterministic: identical logits every launch), adds the bias and selects the
+// top K by rank + softmax. No global partials, no tickets, no serial warp argmax.
+constexpr int kRcTok = 16, kRcPad = 8, kRcThreads = 256, kRcMaxSplit = 8;
+
+struct RouteGeom {
+  int S, kc;
+  size_t smem;
+};
+
+__host__ __device__ inline RouteGeom route_geom(int d_h, int M) {
+  RouteGeom g;
+  int S = (d_h + 255) / 256;
+  if (S > kRcMaxSplit) S = kRcMaxSplit;
+  if (S < 1) S = 1;
+  g.kc = round_up((d_h + S - 1) / S, 16);
+  g.S = (d_h + g.kc - 1) / g.kc;
+  g.smem = static_cast<size_t>(kRcTok + M) * (g.kc + kRcPad) * 2 + static_cast<size_t>(kRcTok) * M * 4;
+  return g;
+}
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                                uint32_t b0, uint32_t b1) {
@@ -110,49 +128,105 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(256) route_mma_kernel(const __nv_bfloat16* __restrict__ x,
-                                                        const __nv_bfloat16* __restrict__ wr,
-                                                        const float* __restrict__ bias, int T, int d_h, int M, int K,
-                                                        int nsplit, float* __restrict__ part,
-                                                        int32_t* __restrict__ tickets, int32_t* __restrict__ ids,
-                                                        float* __restrict__ weights, float* __restrict__ logits_out) {
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// arrive/wait without memory ordering: used where every cross-CTA data dependency is
+// already ordered by an mbarrier (the final "nobody exits early" barrier)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(const void* local_ptr, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_ptr)), "r"(rank));
+  return remote;
+}
+// bulk copy of this CTA's shared memory into another CTA's shared memory (same cluster);
+// completion is counted on the destination CTA's mbarrier
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, const void* src, uint32_t bytes,
+                                               uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+long long* g_route_dbg = nullptr;  // sere_debug_set_route_clocks: per-CTA phase clock64 [cta][8]
+#define RC_PROBE(i) do { if (dbg && threadIdx.x == 0) dbg[(blockIdx.x * gridDim.y + blockIdx.y) * 8 + (i)] = clock64(); } while (0)
+
+__global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const __nv_bfloat16* __restrict__ wr,
+                                                                   const float* __restrict__ bias, int T, int d_h,
+                                                                   int M, int K, int kc,
+                                                                   int32_t* __restrict__ ids,
+                                                                   float* __restrict__ weights,
+                                                                   float* __restrict__ logits_out, long long* dbg) {
   extern __shared__ __align__(16) uint8_t rsm[];
-  constexpr int LD = kRtKC + kRtPad;  // padded row (bank-conflict-free fragment loads)
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(rsm);        // [32][LD]
-  __nv_bfloat16* wt = xs + kRtTok * LD;                             // [M][LD]  (W_r transposed)
-  __shared__ int s_last;
-  const int t0 = blockIdx.x * kRtTok, split = blockIdx.y, k0 = split * kRtKC;
-  const int kn = min(kRtKC, d_h - k0);
+  const int LD = kc + kRcPad;  // padded row (bank-conflict-free fragment loads)
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(rsm);  // [16][LD]
+  __nv_bfloat16* wt = xs + kRcTok * LD;                       // [M][LD]  (W_r transposed: expert-major)
+  float* part = reinterpret_cast<float*>(wt + M * LD);         // [16][M] this split's partial logits
+  __shared__ __align__(8) uint64_t s_bar, s_gather;
+  const int S = gridDim.y;
+  const uint32_t split = cluster_ctarank();
+  const int t0 = blockIdx.x * kRcTok, k0 = static_cast<int>(split) * kc;
+  const int kn = max(0, min(kc, d_h - k0));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int CPR = kRtKC / 8;  // 16-B chunks per staged row (d_h % 8 == 0 on this path)
-  for (int i = tid; i < kRtTok * CPR; i += blockDim.x) {
-    const int t = i / CPR, k = (i % CPR) * 8;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (t0 + t < T && k < kn) v = *reinterpret_cast<const uint4*>(x + static_cast<size_t>(t0 + t) * d_h + k0 + k);
-    *reinterpret_cast<uint4*>(xs + t * LD + k) = v;
+  const int nt_valid = min(kRcTok, T - t0);
+  const int cpr = kc / 8;
+  if (tid == 0) { mbar_init(&s_bar, 1); mbar_init(&s_gather, 1); fence_mbar_init(); }
+  RC_PROBE(0);
+  for (int i = tid; i < kRcTok * cpr; i += blockDim.x) {  // zero the tails (short K chunk, missing tokens)
+    const int t = i / cpr, k = (i % cpr) * 8;
+    if (t >= nt_valid || k >= kn) *reinterpret_cast<uint4*>(xs + t * LD + k) = make_uint4(0u, 0u, 0u, 0u);
   }
-  for (int i = tid; i < M * CPR; i += blockDim.x) {  // W_r^T rows: expert-major, K contiguous
-    const int e = i / CPR, k = (i % CPR) * 8;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (k < kn) v = *reinterpret_cast<const uint4*>(wr + static_cast<size_t>(e) * d_h + k0 + k);
-    *reinterpret_cast<uint4*>(wt + e * LD + k) = v;
-  }
+  if (kn < kc)
+    for (int i = tid; i < M * cpr; i += blockDim.x) {
+      const int e = i / cpr, k = (i % cpr) * 8;
+      if (k >= kn) *reinterpret_cast<uint4*>(wt + e * LD + k) = make_uint4(0u, 0u, 0u, 0u);
+    }
   __syncthreads();
+  RC_PROBE(1);
+  // stage x rows and W_r^T rows of this K chunk with 16-B cp.async (LDGSTS): every thread
+  // keeps all its copies in flight, one memory round trip (small bulk copies would
+  // serialise in the TMA unit: ~150 of 512 B each)
+  {
+    const int rows = nt_valid + M;
+    const int cpn = kn / 8;  // 16-B chunks per row in this K chunk
+    for (int i = tid; i < rows * cpn; i += blockDim.x) {
+      const int r = i / cpn, c = (i % cpn) * 8;
+      const __nv_bfloat16* src = r < nt_valid ? x + static_cast<size_t>(t0 + r) * d_h + k0 + c
+                                              : wr + static_cast<size_t>(r - nt_valid) * d_h + k0 + c;
+      __nv_bfloat16* dst = r < nt_valid ? xs + r * LD + c : wt + (r - nt_valid) * LD + c;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  RC_PROBE(2);
+  }
+  // MMA: the 16 tokens x M experts; warp w takes n-tiles w, w+8, ... (M <= 256: 4 per warp)
+  constexpr int kW = kRcThreads / 32, kJ = 32 / kW;
   const int g = lane >> 2, tg = lane & 3;
-  const int th = warp & 1;                 // token half: rows 16*th .. +16
   const int n_tiles = M / 8;
-  float acc[8][4];
+  float acc[kJ][4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const __nv_bfloat16* xa = xs + (16 * th + g) * LD + tg * 2;
-  for (int kk = 0; kk < kRtKC; kk += 16) {
+  for (int j = 0; j < kJ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  const __nv_bfloat16* xa = xs + g * LD + tg * 2;
+  for (int kk = 0; kk < kc; kk += 16) {
     const uint32_t a0 = *reinterpret_cast<const uint32_t*>(xa + kk);
     const uint32_t a1 = *reinterpret_cast<const uint32_t*>(xa + 8 * LD + kk);
     const uint32_t a2 = *reinterpret_cast<const uint32_t*>(xa + kk + 8);
     const uint32_t a3 = *reinterpret_cast<const uint32_t*>(xa + 8 * LD + kk + 8);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int nt = (warp >> 1) + 4 * j;
+    for (int j = 0; j < kJ; ++j) {
+      const int nt = warp + kW * j;
       if (nt < n_tiles) {
         const __nv_bfloat16* wb = wt + (nt * 8 + g) * LD + tg * 2 + kk;
         const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wb);
@@ -162,96 +236,126 @@ __global__ void __launch_bounds__(256) route_mma_kernel(const __nv_bfloat16* __r
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int nt = (warp >> 1) + 4 * j;
+  for (int j = 0; j < kJ; ++j) {
+    const int nt = warp + kW * j;
     if (nt < n_tiles) {
       const int e = nt * 8 + tg * 2;
-      const int ta = t0 + 16 * th + g, tb = ta + 8;
-      float* pp = part + static_cast<size_t>(split) * T * M;
-      if (ta < T) { pp[static_cast<size_t>(ta) * M + e] = acc[j][0]; pp[static_cast<size_t>(ta) * M + e + 1] = acc[j][1]; }
-      if (tb < T) { pp[static_cast<size_t>(tb) * M + e] = acc[j][2]; pp[static_cast<size_t>(tb) * M + e + 1] = acc[j][3]; }
+      part[g * M + e] = acc[j][0];
+      part[g * M + e + 1] = acc[j][1];
+      part[(g + 8) * M + e] = acc[j][2];
+      part[(g + 8) * M + e + 1] = acc[j][3];
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(&tickets[blockIdx.x], 1) == nsplit - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int tl = warp; tl < kRtTok; tl += blockDim.x / 32) {
-    const int t = t0 + tl;
-    if (t >= T) break;
-    float lg[8];
+  RC_PROBE(3);
+  // exchange: the tile's tokens are spread over the cluster (CTA q owns tokens
+  // [q*tpc, (q+1)*tpc)); every CTA bulk-copies each owner its rows of this split's partial
+  // over distributed shared memory (S-1 copies per CTA, into the owner's idle staging
+  // buffer), then every CTA reduces and ranks its own tokens -- the whole cluster works
+  // on the top-K instead of one warp per token in one CTA
+  const int tpc = (kRcTok + S - 1) / S;
+  const int my_t0 = static_cast<int>(split) * tpc;
+  const int my_rows = max(0, min(tpc, nt_valid - my_t0));
+  float* gath = reinterpret_cast<float*>(rsm);  // [S][tpc][M] (own slot unused)
+  fence_proxy_async_smem();  // generic smem accesses above before the async-proxy copies below
+  if (tid == 0 && my_rows > 0 && S > 1) mbar_arrive_expect_tx(&s_gather, static_cast<uint32_t>(my_rows * M * 4 * (S - 1)));
+  cluster_sync_all();  // partials written, barriers armed, staging buffers no longer read
+  RC_PROBE(4);
+  if (tid < S && tid != static_cast<int>(split)) {
+    const int d = tid;
+    const int rows_d = max(0, min(tpc, nt_valid - d * tpc));
+    if (rows_d > 0)
+      bulk_s2cluster(mapa_shared(gath + (static_cast<int>(split) * tpc) * M, d), part + d * tpc * M,
+                     static_cast<uint32_t>(rows_d * M * 4), mapa_shared(&s_gather, d));
+  }
+  if (my_rows > 0) {
+    if (S > 1) mbar_wait(&s_gather, 0);
+    RC_PROBE(6);
+    float* lgt = part + my_t0 * M;  // my tokens' logits, summed in place
+    for (int i = tid; i < my_rows * M; i += blockDim.x) {
+      const int r = i / M;
+      const float b = bias ? __ldg(bias + i % M) : 0.f;
+      float pv[kRcMaxSplit];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int v = lane + 32 * j;
-      float s = -CUDART_INF_F;
-      if (v < M) {
-        s = 0.f;
-        for (int q = 0; q < nsplit; ++q) s += __ldcg(part + (static_cast<size_t>(q) * T + t) * M + v);
-        if (bias) s += bias[v];
-        if (logits_out) logits_out[static_cast<size_t>(t) * M + v] = s;
-      }
-      lg[j] = s;
+      for (int q = 0; q < kRcMaxSplit; ++q)
+        pv[q] = q >= S ? 0.f : (q == static_cast<int>(split) ? lgt[i] : gath[(q * tpc + r) * M + (i % M)]);
+      float acc_l = 0.f;
+#pragma unroll
+      for (int q = 0; q < kRcMaxSplit; ++q)
+        if (q < S) acc_l += pv[q];  // split order
+      if (bias) acc_l += b;
+      lgt[i] = acc_l;
+      if (logits_out) logits_out[static_cast<size_t>(t0 + my_t0) * M + i] = acc_l;
     }
-    float top = 0.f, den = 0.f, my_w = 0.f;
-    int my_id = 0;
-    for (int r = 0; r < K; ++r) {
-      float bv = -CUDART_INF_F;
-      int bi = -1;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int v = lane + 32 * j;
-        if (v < M && (bi < 0 || lg[j] > bv)) { bv = lg[j]; bi = v; }
+    __syncthreads();
+    RC_PROBE(7);
+    // top-K by rank: candidate v of token r is selected at position rank(v) = #{u : l_u > l_v
+    // or (l_u == l_v and u < v)} < K -- descending, ties to the lower index (moe.py:260)
+    float* sel_v = gath;                                        // [my_rows][K] (gath slot of this CTA)
+    int* sel_i = reinterpret_cast<int*>(gath + my_rows * K);  // [my_rows][K]
+    for (int i = tid; i < my_rows * M; i += blockDim.x) {
+      const int r = i / M, v = i % M;
+      const float lv = lgt[i];
+      const float4* row = reinterpret_cast<const float4*>(lgt + r * M);
+      int rank = 0;
+      for (int u4 = 0; u4 < M / 4; ++u4) {
+        const float4 q4 = row[u4];
+        const int u = u4 * 4;
+        rank += (q4.x > lv) | ((q4.x == lv) & (u < v));
+        rank += (q4.y > lv) | ((q4.y == lv) & (u + 1 < v));
+        rank += (q4.z > lv) | ((q4.z == lv) & (u + 2 < v));
+        rank += (q4.w > lv) | ((q4.w == lv) & (u + 3 < v));
       }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
-      }
-      if (r == 0) top = bv;
-      const float ex = expf(bv - top);
-      den += ex;
-      if (lane == r) { my_id = bi; my_w = ex; }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (lane + 32 * j == bi) lg[j] = -CUDART_INF_F;
+      if (rank < K) { sel_v[r * K + rank] = lv; sel_i[r * K + rank] = v; }
     }
-    if (lane < K) {
-      ids[static_cast<size_t>(t) * K + lane] = my_id;
-      weights[static_cast<size_t>(t) * K + lane] = my_w / den;
+    __syncthreads();
+    for (int r = warp; r < my_rows; r += blockDim.x / 32) {  // softmax over the K picks (moe.py:261-264)
+      const float top = sel_v[r * K];
+      float den = 0.f;
+      for (int k = 0; k < K; ++k) den += __expf(sel_v[r * K + k] - top);
+      if (lane < K) {
+        const size_t o = static_cast<size_t>(t0 + my_t0 + r) * K + lane;
+        ids[o] = sel_i[r * K + lane];
+        weights[o] = __expf(sel_v[r * K + lane] - top) / den;
+      }
     }
   }
-  if (tid == 0) tickets[blockIdx.x] = 0;
+  cluster_sync_relaxed();  // no CTA leaves before the copies out of its shared memory landed
+  RC_PROBE(5);
 }
 
-size_t route_workspace_bytes(int T, int d_h, int M) {
-  const int nsplit = (d_h + kRtKC - 1) / kRtKC;
-  const int tiles = (T + kRtTok - 1) / kRtTok;
-  return 256 + static_cast<size_t>(tiles) * 4 + static_cast<size_t>(nsplit) * T * M * 4;
-}
+size_t route_workspace_bytes(int T, int d_h, int M) { return 256; }
 
-bool route_fast_path(int M, int K, int d_h) { return M % 8 == 0 && M <= 256 && K <= 32 && d_h % 8 == 0; }
+bool route_fast_path(int M, int K, int d_h) {
+  return M % 8 == 0 && M <= 256 && K <= 32 && d_h % 8 == 0 && route_geom(d_h, M).smem <= 200 * 1024;
+}
 
 cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
                              int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out, void* ws,
                              cudaStream_t stream) {
-  const int nsplit = (d_h + kRtKC - 1) / kRtKC;
-  const int tiles = (T + kRtTok - 1) / kRtTok;
-  int32_t* tickets = reinterpret_cast<int32_t*>(ws);
-  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ((tiles * 4 + 255) / 256) * 256);
-  const size_t smem = static_cast<size_t>(kRtTok + M) * (kRtKC + kRtPad) * 2;
+  (void)ws;
+  if (T <= 0) return cudaSuccess;
+  const RouteGeom g = route_geom(d_h, M);
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(route_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  if (g.smem > 48 * 1024 && g.smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(route_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(g.smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured = g.smem;
   }
-  route_mma_kernel<<<dim3(tiles, nsplit), 256, smem, stream>>>(x, w_router, bias, T, d_h, M, K, nsplit, part,
-                                                               tickets, ids, weights, logits_out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((T + kRcTok - 1) / kRcTok, g.S, 1);
+  cfg.blockDim = dim3(kRcThreads, 1, 1);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = g.S;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, route_cluster_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
+                            logits_out, g_route_dbg);
 }
 
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
@@ -279,18 +383,17 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
 }
 
 // ------------------------------------------------------------ residual + RMSNorm
-// x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token. The traversal
-// (4-element chunks per thread, same block size) and the reduction tree are exactly those
-// of the combine kernel's fused epilogue (layout.cu), so the unfused expert-parallel step
-// reproduces the fused single-GPU step bit for bit.
+// x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token with the
+// traversal and reduction tree of the combine kernel's fused epilogue (rowops.cuh), so
+// the unfused expert-parallel step reproduces the fused single-GPU step bit for bit.
 __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
                                                                __nv_bfloat16* __restrict__ h, int d_h, float eps) {
   __shared__ float s_red[8];
   const int t = blockIdx.x;
   float ss = 0.f;
-  for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
+  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
     const size_t o = static_cast<size_t>(t) * d_h + f0;
-    for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+    for (int q = 0; q < kRowVec && f0 + q < d_h; ++q) {
       float v = x[o + q];
       if (y) {
         v = v + y[o + q];
@@ -299,24 +402,17 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
       ss = fmaf(v, v, ss);
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-  for (int i = 0; i < (blockDim.x + 31) / 32; ++i) tot += s_red[i];
+  const float tot = block_sum(ss, s_red);
   const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
-  for (int f0 = threadIdx.x * 4; f0 < d_h; f0 += blockDim.x * 4) {
+  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
     const size_t o = static_cast<size_t>(t) * d_h + f0;
-    for (int q = 0; q < 4 && f0 + q < d_h; ++q) h[o + q] = __float2bfloat16_rn(x[o + q] * r);
+    for (int q = 0; q < kRowVec && f0 + q < d_h; ++q) h[o + q] = __float2bfloat16_rn(x[o + q] * r);
   }
 }
 
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
                                     cudaStream_t stream) {
-  int threads = d_h / 4 >= 256 ? 256 : ((d_h / 4 + 31) / 32) * 32;  // == launch_combine
-  if (threads < 32) threads = 32;
-  residual_rmsnorm_kernel<<<T, threads, 0, stream>>>(x, y, h_out, d_h, eps);
+  residual_rmsnorm_kernel<<<T, row_threads(d_h), 0, stream>>>(x, y, h_out, d_h, eps);
   return cudaGetLastError();
 }
 
