@@ -17,9 +17,10 @@
 //  * weights live in the bank as contiguous 16 KB pre-swizzled tiles (one bulk async
 //    copy each, TMA engine); activations come from the grouped swizzled buffers
 //    (L2-resident, evict-last);
-//  * shared memory is a FIFO ring of 13 x 16 KB pages; a k-step takes mw + 1..2
-//    consecutive pages and one (full, empty) mbarrier pair from an 8-entry ring, so the
-//    stream never drains across unit boundaries and needs one commit per k-step;
+//  * shared memory is a ring of 13 x 16 KB pages; a pipeline step covers kKT k-tiles (1):
+//    their B tiles and the unit's A tiles, consecutive pages, one (full, empty) mbarrier
+//    pair from an 8-entry ring and one commit, so the stream never drains across unit
+//    boundaries;
 //  * TMEM is a ring of columns: a unit takes mw * n_mma columns, the MMA of the next
 //    unit starts as soon as no in-flight unit (4 unit slots, released in order by the
 //    epilogue) holds its columns, so epilogues overlap MMAs whenever two units fit;
@@ -121,10 +122,16 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
   return U;
 }
 
-// A tiles of one k-step: a gate and an up tile per gate/up feature block, one per down m-tile
+#ifndef SERE_KT
+#define SERE_KT 1
+#endif
+constexpr int kKT = SERE_KT;  // 64-wide k-tiles per pipeline step (1: finest-grained page release; 2 measured slower)
+// A tiles (= TMEM accumulators) of one k-tile: gate and up per gate/up feature block, one per down m-tile
 __device__ __forceinline__ int kstep_atiles(const Unit& U) { return U.dn ? U.mwu : 2 * U.mwu; }
-// pages of one k-step: the B tile (1 page up to 128 rows, 2 up to 256) then the A tiles
-__device__ __forceinline__ int kstep_pages(const Unit& U) { return (U.n_mma > 128 ? 2 : 1) + kstep_atiles(U); }
+// pages of the B tile of one k-tile (1 up to 128 rows, 2 up to 256)
+__device__ __forceinline__ int ktile_bpages(const Unit& U) { return U.n_mma > 128 ? 2 : 1; }
+// pages of a step of nk k-tiles: the nk B tiles, then per m-tile block j its nk k-tiles' A tiles
+__device__ __forceinline__ int kstep_pages(const Unit& U, int nk) { return nk * (ktile_bpages(U) + kstep_atiles(U)); }
 
 __device__ __forceinline__ bool ranges_overlap(int a, int na, int b, int nb) { return a < b + nb && b < a + na; }
 
@@ -228,10 +235,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           b_base = p.x_pack;
         }
         if (ut) ut[2] = globaltimer_ns();
-        const int np = kstep_pages(U), bp = np - kstep_atiles(U);
+        const int bpk = ktile_bpages(U);
         const uint32_t b_bytes = static_cast<uint32_t>(U.n_mma) * 128u;
-        const uint32_t tx = b_bytes + ((p.dbg_mode & 1) ? 0u : static_cast<uint32_t>(U.mwu) * a_copy);
-        for (int kt = U.kt_begin; kt < U.kt_end; ++kt, ++kstep) {
+        for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
+          const int nk = min(kKT, U.kt_end - kt);
+          const int np = kstep_pages(U, nk), bp = nk * bpk;
+          const uint32_t tx = nk * (b_bytes + ((p.dbg_mode & 1) ? 0u : static_cast<uint32_t>(U.mwu) * a_copy));
           if (head + np > kPages) head = 0;
           // release in FIFO order until this k-step's entry and pages are free of every
           // in-flight k-step (after a wrap the overlap can be with the youngest ones)
@@ -249,11 +258,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           tail->e_np[e] = np;
           uint8_t* pg = smem + head * kPageBytes;
           mbar_arrive_expect_tx(&tail->full[e], tx);
-          bulk_g2s(pg, b_base + (static_cast<size_t>(kt) * p.r_max + U.row0) * 128, b_bytes, &tail->full[e], pol_x);
-          if (!(p.dbg_mode & 1)) {
+          for (int kk = 0; kk < nk; ++kk)
+            bulk_g2s(pg + kk * bpk * kPageBytes, b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128,
+                     b_bytes, &tail->full[e], pol_x);
+          if (!(p.dbg_mode & 1)) {  // the unit's m-tile j at k-tiles kt..kt+nk-1: one contiguous copy
             const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
             for (int j = 0; j < U.mwu; ++j)
-              bulk_g2s(pg + bp * kPageBytes + j * a_copy, a_kt + j * a_mt_stride, a_copy, &tail->full[e], pol_w);
+              bulk_g2s(pg + bp * kPageBytes + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy, &tail->full[e],
+                       pol_w);
           }
           head += np;
         }
@@ -295,23 +307,30 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         tail->t_col[iter % kTq] = col;
         tail->t_need[iter % kTq] = need;
         tc_fence_after();
-        const int np = kstep_pages(U), bp = np - na;
+        const int bpk = ktile_bpages(U), apj = U.dn ? 1 : 2;  // A tiles per m-tile block and k-tile
         const uint32_t idesc = umma_idesc_bf16(128, U.n_mma);
         const uint32_t d0 = tmem_base + col;
-        for (int kt = U.kt_begin; kt < U.kt_end; ++kt, ++kstep) {
+        for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
+          const int nk = min(kKT, U.kt_end - kt);
+          const int np = kstep_pages(U, nk), bp = nk * bpk;
           if (head + np > kPages) head = 0;
           const int e = kstep % kEntries;
           mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u, acc_full);
           tc_fence_after();
-          const uint32_t b_addr = smem_u32(smem + head * kPageBytes);
+          const uint32_t pg_addr = smem_u32(smem + head * kPageBytes);
           if (!(p.dbg_mode & 2)) {
-            for (int j = 0; j < na; ++j) {  // A tile j -> accumulator j (gate/up: 2f = gate, 2f+1 = up)
-              const uint32_t a_addr = b_addr + (bp + j) * kPageBytes;
-              const uint32_t dj = d0 + j * U.n_mma;
+            for (int kk = 0; kk < nk; ++kk) {
+              const uint32_t b_addr = pg_addr + kk * bpk * kPageBytes;
+              for (int j = 0; j < U.mwu; ++j) {
+                for (int s2 = 0; s2 < apj; ++s2) {  // accumulator j*apj + s2 (gate/up: gate then up)
+                  const uint32_t a_addr = pg_addr + (bp + (j * nk + kk) * apj + s2) * kPageBytes;
+                  const uint32_t dj = d0 + (j * apj + s2) * U.n_mma;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t acc = (kt > U.kt_begin || k > 0) ? 1u : 0u;
-                umma_bf16(dj, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc, acc);
+                  for (int k = 0; k < 4; ++k) {
+                    const uint32_t acc = (kt + kk > U.kt_begin || k > 0) ? 1u : 0u;
+                    umma_bf16(dj, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc, acc);
+                  }
+                }
               }
             }
           }

@@ -166,19 +166,18 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 // Optional decode-block epilogue (x_res != null): x_res[t] += y[t], then
 // h_next[t] = bf16(x_res[t] * rsqrt(mean(x_res[t]^2) + eps)) -- the residual add and the
 // next layer's RMSNorm fused into the same pass over the token row.
-// One CTA per token (rowops.cuh traversal); each thread gathers its 8 features of up to
-// kCombBatch slots at once so that many loads are in flight.
+// One CTA per token (rowops.cuh traversal); the token's slot rows and weights are staged
+// in shared memory once, then each thread gathers its 8 features of kCombBatch slots at
+// a time (16 independent 16-B loads in flight).
 constexpr int kCombBatch = 4;
 
-__device__ __forceinline__ void load_y8(const float* src, int ksplit, size_t split_stride, float (&v)[8]) {
-  float4 a = *reinterpret_cast<const float4*>(src), b = *reinterpret_cast<const float4*>(src + 4);
+__device__ __forceinline__ float4 load_y4(const float* src, int ksplit, size_t split_stride) {
+  float4 a = __ldcg(reinterpret_cast<const float4*>(src));
   for (int s = 1; s < ksplit; ++s) {
-    const float4 oa = *reinterpret_cast<const float4*>(src + s * split_stride);
-    const float4 ob = *reinterpret_cast<const float4*>(src + s * split_stride + 4);
-    a.x = __fadd_rn(a.x, oa.x); a.y = __fadd_rn(a.y, oa.y); a.z = __fadd_rn(a.z, oa.z); a.w = __fadd_rn(a.w, oa.w);
-    b.x = __fadd_rn(b.x, ob.x); b.y = __fadd_rn(b.y, ob.y); b.z = __fadd_rn(b.z, ob.z); b.w = __fadd_rn(b.w, ob.w);
+    const float4 o = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride));
+    a.x = __fadd_rn(a.x, o.x); a.y = __fadd_rn(a.y, o.y); a.z = __fadd_rn(a.z, o.z); a.w = __fadd_rn(a.w, o.w);
   }
-  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  return a;
 }
 
 __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
@@ -189,69 +188,107 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
                                                       float* __restrict__ x_res, __nv_bfloat16* __restrict__ h_next,
                                                       float eps) {
   __shared__ float s_red[8];
+  __shared__ int s_row[64];
+  __shared__ float s_w[64];
   if (plan[P_STATUS] != 0) return;
   const int TK = T * K;
   const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
   const int t = blockIdx.x;
+  const int nslot = K + n_shared;  // <= 32 + 31
+  for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+    s_row[k] = k < K ? slot_row[t * K + k] : slot_row[TK + t * n_shared + (k - K)];
+    s_w[k] = k < K ? w[t * K + k] : 1.f;
+  }
+  __syncthreads();
+  const bool vec4 = (d_h & 3) == 0;
   float ss = 0.f;
-  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
-    // y_perm rows are d_h_pad (multiple of 128) wide, so the 8-float read never leaves the row
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int k0 = 0; k0 < K + n_shared; k0 += kCombBatch) {
-      int row[kCombBatch];
-      float wk[kCombBatch];
-      float v[kCombBatch][8];
+  for (int base = 0; base < d_h; base += blockDim.x * kRowVec) {
+    // y_perm rows are d_h_pad (multiple of 128) wide, so the 4-float reads never leave the row
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int k0 = 0; k0 < nslot; k0 += kCombBatch) {
+      float4 v[kCombBatch][2];
 #pragma unroll
       for (int b = 0; b < kCombBatch; ++b) {
         const int k = k0 + b;
-        row[b] = -1;
-        wk[b] = 1.f;
-        if (k < K) {
-          row[b] = slot_row[t * K + k];
-          wk[b] = w[t * K + k];
-        } else if (k < K + n_shared) {
-          row[b] = slot_row[TK + t * n_shared + (k - K)];
+        const int row = k < nslot ? s_row[k] : -1;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int f = row_chunk(base, c);
+          v[b][c] = (row >= 0 && f < d_h_pad)
+                        ? load_y4(y_perm + static_cast<size_t>(row) * d_h_pad + f, ksplit, split_stride)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        if (row[b] >= 0) load_y8(y_perm + static_cast<size_t>(row[b]) * d_h_pad + f0, ksplit, split_stride, v[b]);
       }
 #pragma unroll
       for (int b = 0; b < kCombBatch; ++b) {
-        if (row[b] < 0) continue;  // padding of the batch, or an expert owned by another rank (EP)
-        if (k0 + b < K) {
+        const int k = k0 + b;
+        if (k >= nslot || s_row[k] < 0) continue;  // batch padding, or an expert owned by another rank (EP)
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wk[b], v[b][q]));
-        } else {  // shared experts: weight 1 (moe.py:308-309)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], v[b][q]);
+        for (int c = 0; c < 2; ++c) {
+          float* a = acc[c];
+          if (k < K) {  // routed slot: products and sums rounded separately, slot order (moe.py:302-307)
+            const float wk = s_w[k];
+            a[0] = __fadd_rn(a[0], __fmul_rn(wk, v[b][c].x));
+            a[1] = __fadd_rn(a[1], __fmul_rn(wk, v[b][c].y));
+            a[2] = __fadd_rn(a[2], __fmul_rn(wk, v[b][c].z));
+            a[3] = __fadd_rn(a[3], __fmul_rn(wk, v[b][c].w));
+          } else {  // shared experts: weight 1 (moe.py:308-309)
+            a[0] = __fadd_rn(a[0], v[b][c].x);
+            a[1] = __fadd_rn(a[1], v[b][c].y);
+            a[2] = __fadd_rn(a[2], v[b][c].z);
+            a[3] = __fadd_rn(a[3], v[b][c].w);
+          }
         }
       }
     }
-    const size_t o = static_cast<size_t>(t) * d_h + f0;
-    const bool full = f0 + 8 <= d_h && (d_h & 3) == 0;
-    if (y) {
-      if (full) {
-        *reinterpret_cast<float4*>(y + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        *reinterpret_cast<float4*>(y + o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-      } else {
-        for (int q = 0; q < 8 && f0 + q < d_h; ++q) y[o + q] = acc[q];
-      }
-    }
-    if (y_bf16)
-      for (int q = 0; q < 8 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[q]);
-    if (x_res) {
-      for (int q = 0; q < 8 && f0 + q < d_h; ++q) {
-        const float vv = x_res[o + q] + acc[q];
-        x_res[o + q] = vv;
-        ss = fmaf(vv, vv, ss);
-      }
-    }
-  }
-  if (x_res) {
-    const float tot = block_sum(ss, s_red);
-    const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
-    for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int f0 = row_chunk(base, c);
+      if (f0 >= d_h) continue;
       const size_t o = static_cast<size_t>(t) * d_h + f0;
-      for (int q = 0; q < 8 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(x_res[o + q] * r);
+      const bool full = vec4 && f0 + 4 <= d_h;
+      if (y) {
+        if (full) *reinterpret_cast<float4*>(y + o) = make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
+        else for (int q = 0; q < 4 && f0 + q < d_h; ++q) y[o + q] = acc[c][q];
+      }
+      if (y_bf16) {
+        if (full) store_bf16x4(y_bf16 + o, acc[c]);
+        else for (int q = 0; q < 4 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[c][q]);
+      }
+      if (x_res) {
+        for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+          const float vv = x_res[o + q] + acc[c][q];
+          x_res[o + q] = vv;
+          acc[c][q] = vv;
+          ss = fmaf(vv, vv, ss);
+        }
+      }
+    }
+    if (x_res && base + static_cast<int>(blockDim.x) * kRowVec >= d_h) {
+      // single-block rows (d_h <= 8 * nthreads, the common case): normalise from registers
+      const float tot = block_sum(ss, s_red);
+      const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
+      if (base == 0) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int f0 = row_chunk(base, c);
+          if (f0 >= d_h) continue;
+          const size_t o = static_cast<size_t>(t) * d_h + f0;
+          float hv[4] = {acc[c][0] * r, acc[c][1] * r, acc[c][2] * r, acc[c][3] * r};
+          if (vec4 && f0 + 4 <= d_h) store_bf16x4(h_next + o, hv);
+          else for (int q = 0; q < 4 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(hv[q]);
+        }
+        return;
+      }
+      for (int b2 = 0; b2 < d_h; b2 += blockDim.x * kRowVec)
+        for (int c = 0; c < 2; ++c) {
+          const int f0 = row_chunk(b2, c);
+          for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+            const size_t o = static_cast<size_t>(t) * d_h + f0 + q;
+            h_next[o] = __float2bfloat16_rn(x_res[o] * r);
+          }
+        }
+      return;
     }
   }
 }

@@ -29,6 +29,7 @@ namespace sere {
 constexpr int kAlignThreads = 1024;
 constexpr int kAlignWarps = kAlignThreads / 32;
 constexpr int kTokBlk = 32;  // tokens per warp block in the rank pass (lane = token)
+constexpr int kMaxGroupsSched = 320;  // >= max bank experts + shared experts (capi.cu kMaxExperts + kMaxShared)
 #define SERE_PHASE(i) do { if (p.dbg && threadIdx.x == 0) p.dbg[(i)] = clock64(); } while (0)
 
 // M = global expert count (ids, sim, classes); Et = local groups (bank experts + shared)
@@ -43,6 +44,14 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb
   b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_need, s_cls
   return round_up(static_cast<int>(b), 16);
+}
+constexpr size_t kAlignSmemCap = 200 * 1024;
+// + the row -> token table staged in shared memory (written out coalesced) when it fits
+__host__ __device__ inline bool align_stage_rows(int T, int K, int M, int Et, int r_max) {
+  return r_max > 0 && align_smem_bytes(T, K, M, Et) + static_cast<size_t>(r_max) * 4 <= kAlignSmemCap;
+}
+__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et, int r_max) {
+  return align_smem_bytes(T, K, M, Et) + (align_stage_rows(T, K, M, Et, r_max) ? static_cast<size_t>(r_max) * 4 : 0);
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -361,30 +370,35 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     }
   }
   __syncthreads();
+  SERE_PHASE(10);
   // schedule order of the fused FFN: padded rows descending, ties by group index (a
   // unit's cost grows with its column count, so this is longest-processing-time first)
   const int G = s_ngroups;
+  __shared__ int s_ugu[kMaxGroupsSched], s_udn[kMaxGroupsSched];  // work units per schedule position
   for (int g = tid; g < G; g += nthr) {
     const int key = s_gpad[g];
     int rank = 0;
+#pragma unroll 8
     for (int j = 0; j < G; ++j) {
       const int kj = s_gpad[j];
       rank += (kj > key) | ((kj == key) & (j < g));
     }
     s_sched[rank] = g;
+    s_ugu[rank] = group_units_gu(key, p.tiles_gu);
+    s_udn[rank] = group_units_dn(key, p.tiles_dn, p.ksplit_dn);
     plan[po.sched + rank] = g;
     plan[po.dep + g] = 0;
   }
   __syncthreads();
-  if (warp == 0) {  // unit prefixes over the schedule order
+  SERE_PHASE(11);
+  if (warp == nwarps - 1) {  // unit prefixes over the schedule order (a warp idle in pass 2 for T < 992)
     int gu_base = 0, dn_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
       int ugu = 0, udn = 0;
       if (i < G) {
-        const int n16 = s_gpad[s_sched[i]];
-        ugu = group_units_gu(n16, p.tiles_gu);
-        udn = group_units_dn(n16, p.tiles_dn, p.ksplit_dn);
+        ugu = s_ugu[i];
+        udn = s_udn[i];
       }
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {
@@ -403,42 +417,63 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
   SERE_PHASE(8);
 
-  // ---- pass 2: permuted row of every (token, slot) cell and its inverse
+  // ---- pass 2: permuted row of every (token, slot) cell and its inverse. slot_row goes
+  // out as one vector store per token; row_token is assembled in shared memory and
+  // written out coalesced (a single SM cannot afford T*K scattered 4-B global stores)
+  const bool stage = align_stage_rows(T, K, M, Et, p.r_max);
+  int32_t* s_rt = reinterpret_cast<int32_t*>(smem + align_smem_bytes(T, K, M, Et));
+  int32_t* rt = stage ? s_rt : p.row_token;
+  const bool vec_sr = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(p.slot_row) & 15) == 0;
   for (int t = tid; t < T; t += nthr) {
     const int tb = t / kTokBlk;
-    for (int k = 0; k < K; ++k) {
-      const int c = t * K + k;
-      const int el = local_of(s_ids[k * T + t]);
-      if (el >= 0) {
-        const int row = s_row0[el] + s_cntb[tb * Et + el] + s_rk[k * T + t];
-        p.slot_row[c] = row;
-        p.row_token[row] = t;
-      } else {
-        p.slot_row[c] = -1;  // owned by another rank (expert parallelism): the combine skips it
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      int rows4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        rows4[j] = -1;  // -1: owned by another rank (expert parallelism), the combine skips it
+        if (k < K) {
+          const int el = local_of(s_ids[k * T + t]);
+          if (el >= 0) {
+            rows4[j] = s_row0[el] + s_cntb[tb * Et + el] + s_rk[k * T + t];
+            rt[rows4[j]] = t;
+          }
+        }
       }
+      int32_t* dst = p.slot_row + static_cast<size_t>(t) * K + k0;
+      if (vec_sr) *reinterpret_cast<int4*>(dst) = make_int4(rows4[0], rows4[1], rows4[2], rows4[3]);
+      else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = rows4[j];
     }
     for (int s = 0; s < p.n_shared; ++s) {  // shared experts: every token, in token order
       const int row = s_row0[m_loc + s] + t;
       p.slot_row[TK + t * p.n_shared + s] = row;
-      p.row_token[row] = t;
+      rt[row] = t;
     }
   }
   for (int e = warp; e < Et; e += nwarps) {  // padding rows of each group
     const int cnt = s_cnt[e];
     if (cnt == 0) continue;
     const int pad = round_up(cnt, kRowAlign);
-    if (lane < pad - cnt) p.row_token[s_row0[e] + cnt + lane] = -1;
+    if (lane < pad - cnt) rt[s_row0[e] + cnt + lane] = -1;
+  }
+  if (stage) {
+    __syncthreads();
+    const int R = plan[P_TOTAL_ROWS];
+    for (int i = tid * 4; i < R; i += nthr * 4) {  // R is a multiple of 16
+      *reinterpret_cast<int4*>(p.row_token + i) = *reinterpret_cast<const int4*>(s_rt + i);
+    }
   }
   if (tid == 0) {
     plan[P_STATUS] = SERE_OK;
     if (p.status_dev) *p.status_dev = SERE_OK;
   }
+  SERE_PHASE(9);
 }
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
-  const size_t smem = align_smem_bytes(p.T, p.K, p.M, p.m_local + p.n_shared);
+  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, p.r_max);
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 32 * 1024 && smem > configured) {  // dynamic + ~4 KB static may cross the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(reroute_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;

@@ -391,23 +391,29 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
   __shared__ float s_red[8];
   const int t = blockIdx.x;
   float ss = 0.f;
-  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
-    const size_t o = static_cast<size_t>(t) * d_h + f0;
-    for (int q = 0; q < kRowVec && f0 + q < d_h; ++q) {
-      float v = x[o + q];
-      if (y) {
-        v = v + y[o + q];
-        x[o + q] = v;
+  for (int base = 0; base < d_h; base += blockDim.x * kRowVec)
+    for (int c = 0; c < 2; ++c) {
+      const int f0 = row_chunk(base, c);
+      for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+        const size_t o = static_cast<size_t>(t) * d_h + f0 + q;
+        float v = x[o];
+        if (y) {
+          v = v + y[o];
+          x[o] = v;
+        }
+        ss = fmaf(v, v, ss);
       }
-      ss = fmaf(v, v, ss);
     }
-  }
   const float tot = block_sum(ss, s_red);
   const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
-  for (int f0 = threadIdx.x * kRowVec; f0 < d_h; f0 += blockDim.x * kRowVec) {
-    const size_t o = static_cast<size_t>(t) * d_h + f0;
-    for (int q = 0; q < kRowVec && f0 + q < d_h; ++q) h[o + q] = __float2bfloat16_rn(x[o + q] * r);
-  }
+  for (int base = 0; base < d_h; base += blockDim.x * kRowVec)
+    for (int c = 0; c < 2; ++c) {
+      const int f0 = row_chunk(base, c);
+      for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
+        const size_t o = static_cast<size_t>(t) * d_h + f0 + q;
+        h[o] = __float2bfloat16_rn(x[o] * r);
+      }
+    }
 }
 
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,

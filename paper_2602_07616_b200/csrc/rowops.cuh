@@ -1,9 +1,12 @@
 // rowops.cuh -- per-token row traversal shared by the combine pass (layout.cu) and the
-// standalone residual + RMSNorm (router.cu): one CTA per token, thread t owns the
-// 8-element chunks t, t + nthreads, ... of the row. Both kernels use this exact
-// traversal and reduction tree, so the unfused expert-parallel step reproduces the
-// fused single-GPU step bit for bit.
+// standalone residual + RMSNorm (router.cu): one CTA per token; the row is walked in
+// blocks of nthreads * 8 elements, and inside a block thread t owns the two 4-element
+// chunks starting at 4*t and 4*(nthreads + t) -- every warp-wide 16-B access covers 512
+// contiguous bytes (full sectors). Both kernels use this exact traversal and reduction
+// tree, so the unfused expert-parallel step reproduces the fused single-GPU step bit
+// for bit.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace sere {
@@ -13,6 +16,17 @@ constexpr int kRowVec = 8;
 __host__ __device__ inline int row_threads(int d_h) {
   int t = ((d_h + kRowVec - 1) / kRowVec + 31) / 32 * 32;
   return t < 32 ? 32 : (t > 256 ? 256 : t);
+}
+
+// element offset of chunk c (0/1) of thread tid in the row block starting at `base`
+__device__ __forceinline__ int row_chunk(int base, int c) { return base + (c * blockDim.x + threadIdx.x) * 4; }
+
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst, const float (&v)[4]) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst) = u;
 }
 
 // sum over the block (warp xor tree, then warps in index order); s_red >= 8 floats
