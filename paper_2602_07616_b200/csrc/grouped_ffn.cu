@@ -234,7 +234,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           a_unit = p.w13 + (static_cast<size_t>(U.expert) * p.tiles_gu + U.mt0) * a_mt_stride;
           b_base = p.x_pack;
         }
-        if (ut) ut[2] = globaltimer_ns();
+        if (ut) {  // ticket | weight KB << 24 | n_mma << 44 | down << 53
+          ut[0] = static_cast<unsigned long long>(u) |
+                  (static_cast<unsigned long long>(U.mwu) * a_copy * (U.kt_end - U.kt_begin) / 1024 << 24) |
+                  (static_cast<unsigned long long>(U.n_mma) << 44) | (static_cast<unsigned long long>(U.dn) << 53);
+          ut[2] = globaltimer_ns();
+        }
         const int bpk = ktile_bpages(U);
         const uint32_t b_bytes = static_cast<uint32_t>(U.n_mma) * 128u;
         for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {

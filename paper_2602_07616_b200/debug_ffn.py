@@ -50,6 +50,7 @@ def main() -> None:
     lib.sere_debug_set_ffn_mode(0)
     lib.sere_debug_set_ffn_trace(None)
     acts = step.active_counts()
+    unit_bytes = {}  # filled per layer below (weights per unit from the plan is not exported: approximate)
     for l in range(a.layers):
         tr = bufs[l].view(sms, 1024).cpu().numpy().astype(np.int64)
         if tr[:, 0].max() == 0:
@@ -79,6 +80,30 @@ def main() -> None:
         print("   mean per-CTA waits (us): " + ", ".join(f"{k} {v:.1f}" for k, v in w.items())
               + f"; clock {1 / ns_per_cyc:.2f} GHz; k-steps/CTA {tr[:, 810].mean():.0f} -> {span / max(tr[:, 810].mean(), 1):.0f} ns each")
         traces.append(tr)
+        # bandwidth profile: each unit's weight bytes spread uniformly over [first copy, last copy]
+        if len(units):
+            ub = np.zeros(len(units))
+            for i, (c, u, tt, tf, tl, te) in enumerate(units):
+                ub[i] = float((int(u) >> 24) & 0xFFFFF) * 1024.0
+            edges = np.arange(0.0, span / 1e3 + 5.0, 5.0)
+            hist = np.zeros(len(edges) - 1)
+            for (c, u, tt, tf, tl, te), b in zip(units, ub):
+                if tl <= tf:
+                    continue
+                lo = np.clip((edges[:-1] - tf) / (tl - tf), 0, 1)
+                hi = np.clip((edges[1:] - tf) / (tl - tf), 0, 1)
+                hist += (hi - lo) * b
+            print("   issue-rate TB/s per 5us:", " ".join(f"{h / 5e-6 / 1e12:.1f}" for h in hist))
+            kind = np.array([(int(u) >> 53) & 1 for u in units[:, 1]])
+            nm = np.array([(int(u) >> 44) & 0x1FF for u in units[:, 1]])
+            dur = units[:, 4] - units[:, 3]
+            for dn in (0, 1):
+                for lo_n, hi_n in ((0, 48), (48, 96), (96, 160), (160, 257)):
+                    m = (kind == dn) & (nm > lo_n) & (nm <= hi_n)
+                    if m.sum():
+                        print(f"   {'dn' if dn else 'gu'} N({lo_n},{hi_n}]: {int(m.sum())} units, issue span "
+                              f"{dur[m].mean():.1f} us, {ub[m].sum() / max(dur[m].sum(), 1e-9) / 1e3:.1f} GB/s per SM, "
+                              f"ticket->first {(units[m, 3] - units[m, 2]).mean():.2f} us")
         if l == 0 and len(units):
             last = units[np.argsort(units[:, 5])[-8:]]
             print("   last units (cta, ticket, t_ticket, t_first, t_last_copy, t_epi):")
