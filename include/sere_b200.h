@@ -189,6 +189,11 @@ int sere_route_topk(const uint16_t* x, const uint16_t* w_router_t, const float* 
  * ------------------------------------------------------------------------ */
 int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int d_h, float eps, void* stream);
 
+/* Programmatic dependent launch on the layer-chain kernels (default off): each kernel may
+ * become resident while its predecessor drains and waits on-device (griddepcontrol)
+ * before touching shared data. 0 disables (plain stream order). */
+int sere_set_pdl(int enable);
+
 /* Profiling hook: when n == 6, every following layer call on this host thread records
  * events[0..4] before its five stages (align, permute, gate/up GEMM, down GEMM,
  * combine) and events[5] after the last, on the launch stream (cudaEvent_t handles).

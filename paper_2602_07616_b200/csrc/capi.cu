@@ -193,6 +193,10 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 }  // namespace
 }  // namespace sere
 
+namespace sere {
+bool g_pdl = false;  // measured no gain on the C4 step; kept switchable (sere_set_pdl)
+}  // namespace sere
+
 using namespace sere;
 
 extern "C" {
@@ -412,6 +416,11 @@ int sere_debug_set_align_clocks(int64_t* dev_buf) {
 
 int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
   g_ffn_trace = reinterpret_cast<unsigned long long*>(dev_buf);
+  return SERE_OK;
+}
+
+int sere_set_pdl(int enable) {
+  g_pdl = enable != 0;
   return SERE_OK;
 }
 

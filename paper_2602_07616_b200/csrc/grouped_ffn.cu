@@ -55,6 +55,7 @@ constexpr int kEntries = 8;   // k-step barrier ring
 constexpr int kQueue = 4;     // unit-id queue producer -> MMA / epilogue
 constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
 constexpr int kFfnThreads = 192;
+constexpr int kPdlPrefetch = 4;  // k-steps whose weights are issued before waiting on the permute kernel
 static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
 struct Unit {
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   int32_t* dep = plan + po.dep;
   unsigned long long* tr = p.trace ? p.trace + static_cast<size_t>(blockIdx.x) * kFfnTraceStride : nullptr;
   if (tr && threadIdx.x == 0) { tr[0] = globaltimer_ns(); tr[813] = clock64(); }
+  // no early pdl_trigger: a combine grid resident during the FFN measurably slows it down
 
   if (warp == 0) {
     if (lane == 0) {
@@ -197,6 +199,23 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       int qs = 0, nu = 0, head = 0, kstep = 0, oldest = 0;
       uint32_t qph = 0;
       unsigned long long w_empty = 0, w_dep = 0, w_q = 0;
+      // PDL: weights do not depend on the preceding kernel (permute), so the first k-steps'
+      // weight tiles are issued before griddepcontrol.wait; their activation tiles follow it
+      bool pdl_done = false;
+      int n_pend = 0;
+      uint32_t pend_dst[kPdlPrefetch], pend_bytes[kPdlPrefetch], pend_bar[kPdlPrefetch];
+      const uint8_t* pend_src[kPdlPrefetch];
+      auto pdl_flush = [&]() {
+        pdl_wait();
+        for (int i = 0; i < n_pend; ++i)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+              "%4;" ::"r"(pend_dst[i]),
+              "l"(pend_src[i]), "r"(pend_bytes[i]), "r"(pend_bar[i]), "l"(pol_x)
+              : "memory");
+        n_pend = 0;
+        pdl_done = true;
+      };
       unsigned long long* acc_empty = tr ? &w_empty : nullptr;
       for (;; ++nu) {
         const int u = units_total > 0 ? atomicAdd(plan + P_TICKET, 1) : 0;
@@ -225,8 +244,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           }
           fence_proxy_async_global();
           a_copy = kTileBytes;
-          a_mt_stride = static_cast<size_t>(p.ktiles_dn) * a_copy;
-          a_unit = p.w2 + (static_cast<size_t>(U.expert) * p.tiles_dn + U.mt0) * a_mt_stride;
+          a_mt_stride = 0;  // unused: the unit's m-tiles are adjacent per k-tile (w2_tile_offset)
+          a_unit = p.w2 + w2_tile_offset(U.expert, U.mt0, 0, p.tiles_dn, p.ktiles_dn);
           b_base = p.h_pack;
         } else {
           a_copy = 2 * kTileBytes;
@@ -254,6 +273,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
             for (int s2 = oldest; !busy && s2 < kstep; ++s2)
               busy = ranges_overlap(head, np, tail->e_page[s2 % kEntries], tail->e_np[s2 % kEntries]);
             if (!busy) break;
+            // an in-flight k-step can only complete once its deferred activation copy is issued
+            if (!pdl_done) pdl_flush();
             mbar_wait_timed(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u,
                             acc_empty);
             ++oldest;
@@ -263,19 +284,46 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           tail->e_np[e] = np;
           uint8_t* pg = smem + head * kPageBytes;
           mbar_arrive_expect_tx(&tail->full[e], tx);
-          for (int kk = 0; kk < nk; ++kk)
-            bulk_g2s(pg + kk * bpk * kPageBytes, b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128,
-                     b_bytes, &tail->full[e], pol_x);
-          if (!(p.dbg_mode & 1)) {  // the unit's m-tile j at k-tiles kt..kt+nk-1: one contiguous copy
-            const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
-            for (int j = 0; j < U.mwu; ++j)
-              bulk_g2s(pg + bp * kPageBytes + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy, &tail->full[e],
-                       pol_w);
+          if (!(p.dbg_mode & 1)) {
+            if (U.dn) {  // k-tile kk: the unit's 1-2 adjacent m-tiles, one copy (pages kk-major)
+              for (int kk = 0; kk < nk; ++kk) {
+#if SERE_W2_PAIRS
+                bulk_g2s(pg + (bp + kk * U.mwu) * kPageBytes, a_unit + static_cast<size_t>(kt + kk) * 2 * kTileBytes,
+                         U.mwu * kTileBytes, &tail->full[e], pol_w);
+#else
+                for (int j = 0; j < U.mwu; ++j)
+                  bulk_g2s(pg + (bp + kk * U.mwu + j) * kPageBytes,
+                           p.w2 + w2_tile_offset(U.expert, U.mt0 + j, kt + kk, p.tiles_dn, p.ktiles_dn), kTileBytes,
+                           &tail->full[e], pol_w);
+#endif
+              }
+            } else {  // feature block j at k-tiles kt..kt+nk-1: gate/up tiles, one contiguous copy
+              const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
+              for (int j = 0; j < U.mwu; ++j)
+                bulk_g2s(pg + bp * kPageBytes + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy,
+                         &tail->full[e], pol_w);
+            }
+          }
+          if (!pdl_done && (U.dn || n_pend + nk > kPdlPrefetch)) pdl_flush();
+          for (int kk = 0; kk < nk; ++kk) {
+            uint8_t* bdst = pg + kk * bpk * kPageBytes;
+            const uint8_t* bsrc = b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128;
+            if (pdl_done) {
+              bulk_g2s(bdst, bsrc, b_bytes, &tail->full[e], pol_x);
+            } else {
+              pend_dst[n_pend] = smem_u32(bdst);
+              pend_src[n_pend] = bsrc;
+              pend_bytes[n_pend] = b_bytes;
+              pend_bar[n_pend] = smem_u32(&tail->full[e]);
+              ++n_pend;
+            }
           }
           head += np;
         }
+        if (!pdl_done) pdl_flush();
         if (ut) ut[3] = globaltimer_ns();
       }
+      if (!pdl_done) pdl_flush();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -328,7 +376,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
               const uint32_t b_addr = pg_addr + kk * bpk * kPageBytes;
               for (int j = 0; j < U.mwu; ++j) {
                 for (int s2 = 0; s2 < apj; ++s2) {  // accumulator j*apj + s2 (gate/up: gate then up)
-                  const uint32_t a_addr = pg_addr + (bp + (j * nk + kk) * apj + s2) * kPageBytes;
+                  const int apage = U.dn ? bp + kk * U.mwu + j : bp + (j * nk + kk) * apj + s2;
+                  const uint32_t a_addr = pg_addr + apage * kPageBytes;
                   const uint32_t dj = d0 + (j * apj + s2) * U.n_mma;
 #pragma unroll
                   for (int k = 0; k < 4; ++k) {
@@ -407,7 +456,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int jr = c0 + i;
-              if (jr < U.rows_valid)
+              if (jr < U.rows_valid && !(p.dbg_mode & 4))
                 ybase[static_cast<size_t>(U.row0 + jr) * p.d_h_pad + feat] = __uint_as_float(r[i]);
             }
           }
@@ -446,8 +495,7 @@ cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream)
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  moe_ffn_kernel<<<num_sms, kFfnThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(g_pdl, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
 }
 
 size_t moe_ffn_smem(int Et) { return ffn_smem_bytes(Et); }

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(256) pack_w13_kernel(const __nv_bfloat16* __re
   tile_xfer(W, d_h, d_m, fb * 128, kt * 64, dst, unpack, sd);
 }
 
-// W2 tile (e, mt, kt): output features 128*mt.., inputs 64*kt.. of w_down [d_m, d_h]
+// W2 tile (e, mt, kt): output features 128*mt.., inputs 64*kt.. of w_down [d_m, d_h]; placed by
+// w2_tile_offset (m-tile pairs adjacent per k-tile)
 __global__ void __launch_bounds__(256) pack_w2_kernel(const __nv_bfloat16* __restrict__ wd, int d_h, int d_m,
                                                       int tiles, int ktiles, uint8_t* __restrict__ w2, int first,
                                                       int unpack) {
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(256) pack_w2_kernel(const __nv_bfloat16* __res
   const int kt = tile % ktiles;
   const int mt = (tile / ktiles) % tiles;
   const int e = tile / (ktiles * tiles);
-  uint8_t* dst = w2 + (static_cast<size_t>((first + e) * tiles + mt) * ktiles + kt) * kTileBytes;
+  uint8_t* dst = w2 + w2_tile_offset(first + e, mt, kt, tiles, ktiles);
   tile_xfer(wd + static_cast<size_t>(e) * d_m * d_h, d_m, d_h, mt * 128, kt * 64, dst, unpack, sd);
 }
 
@@ -111,6 +112,8 @@ __global__ void __launch_bounds__(256) permute_kernel(const __nv_bfloat16* __res
                                                       const int32_t* __restrict__ plan,
                                                       const int32_t* __restrict__ row_token, int r_max,
                                                       uint8_t* __restrict__ x_pack) {
+  pdl_wait();
+  pdl_trigger();
   if (plan[P_STATUS] != 0) return;
   const int total_rows = plan[P_TOTAL_ROWS];
   const int cpr = d_h_pad / 8;  // 16-B chunks per row
@@ -155,8 +158,8 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
   int blocks = (r_max + 7) / 8;  // one warp per row, 8 warps per CTA
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (blocks < 1) blocks = 1;
-  permute_kernel<<<blocks, 256, 0, stream>>>(x, d.d_h, d.d_h_pad, plan, row_token, r_max, x_pack);
-  return cudaGetLastError();
+  return launch_pdl(g_pdl, permute_kernel, dim3(blocks), dim3(256), 0, stream, x, d.d_h, d.d_h_pad, plan, row_token,
+                    r_max, x_pack);
 }
 
 // ------------------------------------------------------------------ combine
@@ -190,7 +193,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
   __shared__ float s_red[8];
   __shared__ int s_row[64];
   __shared__ float s_w[64];
-  if (plan[P_STATUS] != 0) return;
+  // slot rows / weights / the plan come from kernels that completed before the FFN started;
+  // y_perm (FFN) and x_res (RMW) need the predecessor grid: wait after staging the slots
+  if (plan[P_STATUS] != 0) { pdl_wait(); return; }
   const int TK = T * K;
   const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
   const int t = blockIdx.x;
@@ -200,6 +205,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
     s_w[k] = k < K ? w[t * K + k] : 1.f;
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   const bool vec4 = (d_h & 3) == 0;
   float ss = 0.f;
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec) {
@@ -298,9 +305,8 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
                            cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  combine_kernel<<<T, row_threads(d.d_h), 0, stream>>>(y_perm, d.ksplit_dn, r_max, d.d_h, d.d_h_pad, plan, slot_row,
-                                                        w, T, K, n_shared, y, y_bf16, x_res, h_next, eps);
-  return cudaGetLastError();
+  return launch_pdl(g_pdl, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
+                    d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps);
 }
 
 }  // namespace sere

@@ -1,6 +1,7 @@
 // params.cuh -- launch parameter blocks shared by the kernels and capi.cu.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -45,13 +46,32 @@ struct FfnParams {
   int32_t* plan;          // written by reroute_align; the ticket and dep counters are updated here
   int Et;
   int act;
-  int dbg_mode;               // debug experiments: bit0 skip weight copies, bit1 skip MMAs (results invalid)
+  int dbg_mode;               // debug experiments (results invalid): bit0 skip weight copies, bit1 skip MMAs,
+                              // bit2 skip the expert-output stores
   unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
 };
 constexpr int kFfnTraceStride = 1024;
 constexpr int kFfnTraceUnits = 200;
 
-extern long long* g_route_dbg;  // router.cu: debug phase clocks of the router (nullptr = off)
+extern long long* g_route_dbg;
+
+// launch with programmatic stream serialisation (PDL); `pdl` false = ordinary launch
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+extern bool g_pdl;  // capi.cu: PDL on the layer chain (sere_set_pdl)  // router.cu: debug phase clocks of the router (nullptr = off)
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);

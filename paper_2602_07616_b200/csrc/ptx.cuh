@@ -63,6 +63,15 @@ __device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, 
   *acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
+// ------------------------------------- programmatic dependent launch (PDL)
+// Kernels of the layer chain are launched with programmatic stream serialisation: the
+// next kernel may become resident while this one drains. pdl_wait() blocks until the
+// preceding grid completed and its memory is visible (no-op without PDL); every kernel
+// calls it before touching data produced OR consumed by its predecessors, so completion
+// stays transitive along the chain. pdl_trigger() lets the dependent grid launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------- cross-CTA signalling (global memory)
 __device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
   int v;

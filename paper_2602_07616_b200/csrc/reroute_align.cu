@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     for (int i = tid; i < TB * Et; i += nthr) s_cntb[i] = 0;
   }
   __syncthreads();
+  pdl_wait();  // ids come from the router; outputs are read by the previous layer's kernels
+  pdl_trigger();
   SERE_PHASE(0);
 
   // ---- load + validate ids (rerouting.py:111-114 / moe.py:299-300); lane = token, no div/mod
@@ -479,8 +481,7 @@ cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  reroute_align_kernel<<<1, kAlignThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
 }
 
 size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }

@@ -198,14 +198,21 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
   // keeps all its copies in flight, one memory round trip (small bulk copies would
   // serialise in the TMA unit: ~150 of 512 B each)
   {
-    const int rows = nt_valid + M;
     const int cpn = kn / 8;  // 16-B chunks per row in this K chunk
-    for (int i = tid; i < rows * cpn; i += blockDim.x) {
+    // router weights are static: stage them before waiting on the previous kernel (PDL)
+    for (int i = tid; i < M * cpn; i += blockDim.x) {
       const int r = i / cpn, c = (i % cpn) * 8;
-      const __nv_bfloat16* src = r < nt_valid ? x + static_cast<size_t>(t0 + r) * d_h + k0 + c
-                                              : wr + static_cast<size_t>(r - nt_valid) * d_h + k0 + c;
-      __nv_bfloat16* dst = r < nt_valid ? xs + r * LD + c : wt + (r - nt_valid) * LD + c;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(wt + r * LD + c)),
+                   "l"(wr + static_cast<size_t>(r) * d_h + k0 + c)
+                   : "memory");
+    }
+    pdl_wait();  // x = the previous layer's RMSNorm output; ids/weights are read by its kernels
+    pdl_trigger();
+    for (int i = tid; i < nt_valid * cpn; i += blockDim.x) {
+      const int r = i / cpn, c = (i % cpn) * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(xs + r * LD + c)),
+                   "l"(x + static_cast<size_t>(t0 + r) * d_h + k0 + c)
+                   : "memory");
     }
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncthreads();
@@ -347,13 +354,15 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
   cfg.blockDim = dim3(kRcThreads, 1, 1);
   cfg.dynamicSmemBytes = g.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = g.S;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, route_cluster_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
                             logits_out, g_route_dbg);
 }
@@ -389,6 +398,8 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
 __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
                                                                __nv_bfloat16* __restrict__ h, int d_h, float eps) {
   __shared__ float s_red[8];
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   float ss = 0.f;
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec)
@@ -418,8 +429,7 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
 
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
                                     cudaStream_t stream) {
-  residual_rmsnorm_kernel<<<T, row_threads(d_h), 0, stream>>>(x, y, h_out, d_h, eps);
-  return cudaGetLastError();
+  return launch_pdl(g_pdl, residual_rmsnorm_kernel, dim3(T), dim3(row_threads(d_h)), 0, stream, x, y, h_out, d_h, eps);
 }
 
 }  // namespace sere

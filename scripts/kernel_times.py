@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--mode", default="sere")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--T", type=int, default=512)
+    ap.add_argument("--pdl", type=int, default=1)
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -24,6 +25,8 @@ def main():
     from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
 
     build.build()
+    from paper_2602_07616_b200 import _lib
+    _lib.load().sere_set_pdl(a.pdl)
     model = DecodeModel(a.layers, 128, 8, 2048, 768, seed=0, beta=1.0)
     step = DecodeStep(model, a.T, 1, 0.5, a.mode)
     step.set_input(torch.randn(a.T, 2048, device="cuda"))
