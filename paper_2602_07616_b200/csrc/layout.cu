@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
         }
       }
     }
-    if (x_res && base + static_cast<int>(blockDim.x) * kRowVec >= d_h) {
+    if (x_res && h_next && base + static_cast<int>(blockDim.x) * kRowVec >= d_h) {
       // single-block rows (d_h <= 8 * nthreads, the common case): normalise from registers
       const float tot = block_sum(ss, s_red);
       const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
