@@ -30,7 +30,9 @@
 //    gate/up unit of its group has published h (per-group counters in the plan,
 //    release/acquire + async-proxy fences): no grid barrier, no second launch;
 //  * warp roles: warp 0 = producer (one lane), warp 1 = MMA issuer (one lane, also owns
-//    the TMEM allocation), warps 2..5 = epilogue (TMEM lane quadrants 2,3,0,1). Page,
+//    the TMEM allocation), warps 2..9 = epilogue (TMEM lane quadrant = warp % 4, two
+//    warps per quadrant splitting the 16-column chunks: the fp32 down-output stores
+//    otherwise hold TMEM long enough to stall the MMA issuer). Page,
 //    column and slot positions are pure functions of the unit sequence, so the three
 //    roles recompute them instead of exchanging them.
 // Epilogues:
@@ -54,7 +56,12 @@ constexpr int kPageBytes = 16384;
 constexpr int kEntries = 8;   // k-step barrier ring
 constexpr int kQueue = 4;     // unit-id queue producer -> MMA / epilogue
 constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
-constexpr int kFfnThreads = 192;
+#ifndef SERE_EPI_WARPS
+#define SERE_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = SERE_EPI_WARPS;   // epilogue warps: kEpiWarps/4 per TMEM lane quadrant
+constexpr int kEpiGroups = kEpiWarps / 4;   // warp groups splitting a unit's 16-column chunks
+constexpr int kFfnThreads = 64 + 32 * kEpiWarps;
 constexpr int kPdlPrefetch = 4;  // k-steps whose weights are issued before waiting on the permute kernel
 static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
@@ -161,8 +168,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kEntries; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], 1); }
-    for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], 1); mbar_init(&tail->tempty[i], 4); }
-    for (int i = 0; i < kQueue; ++i) { mbar_init(&tail->q_full[i], 1); mbar_init(&tail->q_empty[i], 1 + 4); }
+    for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], 1); mbar_init(&tail->tempty[i], kEpiWarps); }
+    for (int i = 0; i < kQueue; ++i) { mbar_init(&tail->q_full[i], 1); mbar_init(&tail->q_empty[i], 1 + kEpiWarps); }
     fence_mbar_init();
     tail->n_groups = ng;
     tail->units_gu = status == 0 ? plan[P_UNITS_GU] : 0;
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       const uint64_t pol_x = policy_evict_last();
       int qs = 0, nu = 0, head = 0, kstep = 0, oldest = 0;
       uint32_t qph = 0;
-      unsigned long long w_empty = 0, w_dep = 0, w_q = 0;
+      unsigned long long w_empty = 0, w_dep = 0, w_q = 0, w_empty_dn = 0;
       // PDL: weights do not depend on the preceding kernel (permute), so the first k-steps'
       // weight tiles are issued before griddepcontrol.wait; their activation tiles follow it
       bool pdl_done = false;
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         mbar_arrive(&tail->q_full[qs]);
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (done) {
-          if (tr) { tr[1] = w_empty; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; }
+          if (tr) { tr[1] = w_empty + w_empty_dn; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; tr[1018] = w_empty_dn; }
           break;
         }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
             // an in-flight k-step can only complete once its deferred activation copy is issued
             if (!pdl_done) pdl_flush();
             mbar_wait_timed(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u,
-                            acc_empty);
+                            acc_empty ? (U.dn ? &w_empty_dn : acc_empty) : nullptr);
             ++oldest;
           }
           const int e = kstep % kEntries;
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       // ===================== MMA issuer (single thread)
       int qs = 0, iter = 0, head = 0, kstep = 0, tcol = 0, oldest = 0;
       uint32_t qph = 0;
-      unsigned long long w_full = 0, w_tmem = 0, nks = 0;
+      unsigned long long w_full = 0, w_tmem = 0, nks = 0, w_full_dn = 0, w_tmem_dn = 0, nks_dn = 0;
       unsigned long long* acc_full = tr ? &w_full : nullptr;
       for (;; ++iter) {
         mbar_wait(&tail->q_full[qs], qph);
@@ -338,7 +345,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         mbar_arrive(&tail->q_empty[qs]);
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (u < 0) {
-          if (tr) { tr[2] = w_full; tr[5] = w_tmem; tr[810] = nks; }
+          if (tr) {
+            tr[2] = w_full + w_full_dn; tr[5] = w_tmem + w_tmem_dn; tr[810] = nks;
+            tr[1019] = w_full_dn; tr[1020] = w_tmem_dn; tr[1021] = nks_dn;
+          }
           break;
         }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
             busy = ranges_overlap(col, need, tail->t_col[i2 % kTq], tail->t_need[i2 % kTq]);
           if (!busy) break;
           mbar_wait_timed(&tail->tempty[oldest % kTq], static_cast<uint32_t>(oldest / kTq) & 1u,
-                          tr ? &w_tmem : nullptr);
+                          tr ? (U.dn ? &w_tmem_dn : &w_tmem) : nullptr);
           ++oldest;
         }
         tail->t_col[iter % kTq] = col;
@@ -368,7 +378,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int np = kstep_pages(U, nk), bp = nk * bpk;
           if (head + np > kPages) head = 0;
           const int e = kstep % kEntries;
-          mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u, acc_full);
+          mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u,
+                          acc_full ? (U.dn ? &w_full_dn : acc_full) : nullptr);
+          nks_dn += U.dn;
           tc_fence_after();
           const uint32_t pg_addr = smem_u32(smem + head * kPageBytes);
           if (!(p.dbg_mode & 2)) {
@@ -397,7 +409,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
     }
   } else {
     // ===================== epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
-    const int q = warp & 3;
+    const int q = warp & 3;               // TMEM lane quadrant of this warp
+    const int eg = (warp - 2) / 4;         // column group: chunks c0 = 16 * (eg + kEpiGroups * i)
     int qs = 0, iter = 0, tcol = 0;
     uint32_t qph = 0;
     unsigned long long w_tf = 0;
@@ -430,7 +443,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int fl = f & 63;
           uint8_t* hbase = p.h_pack + static_cast<size_t>(f >> 6) * p.r_max * 128 + (fl & 7) * 2;
           const uint32_t tg = tq + (2 * j) * U.n_mma, tu = tg + U.n_mma;
-          for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
+          for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
             uint32_t rg[16], ru[16];
             tmem_ld16(tg + c0, rg);
             tmem_ld16(tu + c0, ru);
@@ -449,7 +462,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int feat = (U.mt0 + j) * 128 + q * 32 + lane;
           float* ybase = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * p.d_h_pad;
           const uint32_t taddr = tq + j * U.n_mma;
-          for (int c0 = 0; c0 < U.n_mma; c0 += 16) {
+          for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
             uint32_t r[16];
             tmem_ld16(taddr + c0, r);
             tmem_wait_ld();
@@ -470,7 +483,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         // publish this unit's slice of h: the down units of the group (any SM) read it with
         // bulk copies (async proxy) after acquiring the counter
         fence_proxy_async_global();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 32 * kEpiWarps);
         if (warp == 2 && lane == 0) {
           __threadfence();
           atomicAdd(dep + U.g, 1);

@@ -94,6 +94,11 @@ def main() -> None:
                 hi = np.clip((edges[1:] - tf) / (tl - tf), 0, 1)
                 hist += (hi - lo) * b
             print("   issue-rate TB/s per 5us:", " ".join(f"{h / 5e-6 / 1e12:.1f}" for h in hist))
+            cyc = ns_per_cyc / 1e3
+            print(f"   down-phase waits (us/CTA): slot {tr[:, 1018].mean() * cyc:.1f} of {tr[:, 1].mean() * cyc:.1f}, "
+                  f"operand {tr[:, 1019].mean() * cyc:.1f} of {tr[:, 2].mean() * cyc:.1f}, "
+                  f"tmem {tr[:, 1020].mean() * cyc:.1f} of {tr[:, 5].mean() * cyc:.1f}; "
+                  f"down k-steps {tr[:, 1021].mean():.0f} of {tr[:, 810].mean():.0f}")
             kind = np.array([(int(u) >> 53) & 1 for u in units[:, 1]])
             nm = np.array([(int(u) >> 44) & 0x1FF for u in units[:, 1]])
             dur = units[:, 4] - units[:, 3]
