@@ -216,6 +216,11 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf);
 int sere_debug_set_ffn_mode(int mode);
 /* Debug: router phase clocks (clock64) per CTA, dev_buf[cta * 8 + phase]. NULL disables. */
 int sere_debug_set_route_clocks(int64_t* dev_buf);
+/* Kernel-only timing: relaunch the fused expert FFN `reps` times on the plan and operands
+ * the last sere_*forward call left in `workspace` (the FFN re-arms its ticket and
+ * dependency counters when it finishes; outputs are rewritten with identical values). */
+int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, int T, int K,
+                          void* workspace, size_t workspace_bytes, int reps, void* stream);
 
 /* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).

@@ -104,6 +104,34 @@ int check_reroute_cfg(int K, int M, int S, double rho) {
   return SERE_OK;
 }
 
+uint8_t* ws_base(const void* workspace) {
+  return reinterpret_cast<uint8_t*>(align_up(reinterpret_cast<uintptr_t>(workspace), 1024));
+}
+
+FfnParams ffn_params(const void* bank, const WsLayout& L, uint8_t* ws, int activation) {
+  const Dims& d = L.d;
+  const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
+  FfnParams fp{};
+  fp.w13 = w13;
+  fp.w2 = w13 + bank_w13_bytes(L.Et, d);
+  fp.tiles_gu = d.tiles_gu;
+  fp.ktiles_gu = d.ktiles_gu;
+  fp.tiles_dn = d.tiles_dn;
+  fp.ktiles_dn = d.ktiles_dn;
+  fp.ksplit_dn = d.ksplit_dn;
+  fp.x_pack = ws + L.x_pack;
+  fp.h_pack = ws + L.h_pack;
+  fp.y_perm = reinterpret_cast<float*>(ws + L.y_perm);
+  fp.r_max = L.r_max;
+  fp.d_h_pad = d.d_h_pad;
+  fp.plan = reinterpret_cast<int32_t*>(ws + L.plan);
+  fp.Et = L.Et;
+  fp.act = activation;
+  fp.trace = g_ffn_trace;
+  fp.dbg_mode = g_ffn_dbg_mode;
+  return fp;
+}
+
 // M = global expert count; the bank holds global experts [e_lo, e_lo + m_local) + n_shared shared ones
 int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int d_h, int d_m, int activation,
               const double* sim, int S,
@@ -158,25 +186,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
-  const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
-  FfnParams fp{};
-  fp.w13 = w13;
-  fp.w2 = w13 + bank_w13_bytes(L.Et, d);
-  fp.tiles_gu = d.tiles_gu;
-  fp.ktiles_gu = d.ktiles_gu;
-  fp.tiles_dn = d.tiles_dn;
-  fp.ktiles_dn = d.ktiles_dn;
-  fp.ksplit_dn = d.ksplit_dn;
-  fp.x_pack = x_pack;
-  fp.h_pack = h_pack;
-  fp.y_perm = y_perm;
-  fp.r_max = L.r_max;
-  fp.d_h_pad = d.d_h_pad;
-  fp.plan = plan;
-  fp.Et = L.Et;
-  fp.act = activation;
-  fp.trace = g_ffn_trace;
-  fp.dbg_mode = g_ffn_dbg_mode;
+  FfnParams fp = ffn_params(bank, L, ws, activation);
   stage_mark(2, stream);
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -416,6 +426,21 @@ int sere_debug_set_align_clocks(int64_t* dev_buf) {
 
 int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
   g_ffn_trace = reinterpret_cast<unsigned long long*>(dev_buf);
+  return SERE_OK;
+}
+
+int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, int T, int K,
+                          void* workspace, size_t workspace_bytes, int reps, void* stream) {
+  int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
+  if (rc != SERE_OK) return rc;
+  if (!bank || !workspace || reps < 0) return SERE_ERR_DIMENSION;
+  const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
+  if (workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
+  const FfnParams fp = ffn_params(bank, L, ws_base(workspace), activation);
+  for (int i = 0; i < reps; ++i) {
+    const cudaError_t e = launch_moe_ffn(fp, num_sms(), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return SERE_ERR_CUDA;
+  }
   return SERE_OK;
 }
 

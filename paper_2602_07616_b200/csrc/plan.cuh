@@ -10,6 +10,9 @@
 //   plan[P_TOTAL_ROWS]    rows of the permuted batch (each group padded to 16)
 //   plan[P_UNITS_GU/DN]   work units of the gate/up and down phases of the fused FFN
 //   plan[P_TICKET]        work-unit ticket counter of the fused FFN (zeroed by align)
+//   plan[P_DONE]          CTAs of the fused FFN that finished; the last one re-zeroes the
+//                         ticket and dependency counters, so the FFN can be relaunched on
+//                         the same plan (sere_debug_replay_ffn: kernel-only timing)
 //   counts[Et]            cells routed to each bank expert (shared experts: T)
 //   group_expert/row0/rows[Et]   bank expert, first permuted row, valid rows of group g
 //   sched[Et]             groups in schedule order: padded rows descending (heaviest
@@ -31,6 +34,7 @@ enum PlanIdx : int {
   P_UNITS_DN = 4,
   P_NACTIVE = 5,
   P_TICKET = 6,
+  P_DONE = 7,
   P_HDR = 16
 };
 

@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         plan[P_NGROUPS] = g_tot;
         plan[P_TOTAL_ROWS] = r_tot;
         plan[P_TICKET] = 0;
+        plan[P_DONE] = 0;
         if (!reroute) plan[P_NACTIVE] = g_tot - p.n_shared;
       }
     }
