@@ -62,7 +62,10 @@ constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
 constexpr int kEpiWarps = SERE_EPI_WARPS;   // epilogue warps: kEpiWarps/4 per TMEM lane quadrant
 constexpr int kEpiGroups = kEpiWarps / 4;   // warp groups splitting a unit's 16-column chunks
 constexpr int kFfnThreads = 64 + 32 * kEpiWarps;
-constexpr int kPdlPrefetch = 4;  // k-steps whose weights are issued before waiting on the permute kernel
+constexpr int kPdlPrefetch = 4;
+#ifndef SERE_STATIC_FIRST
+#define SERE_STATIC_FIRST 1
+#endif  // k-steps whose weights are issued before waiting on the permute kernel
 static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
 struct Unit {
@@ -225,7 +228,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       };
       unsigned long long* acc_empty = tr ? &w_empty : nullptr;
       for (;; ++nu) {
+        // the first unit of CTA b is ticket b (no atomic round trip before the first copy);
+        // the counter hands out tickets from gridDim.x on
+#if SERE_STATIC_FIRST
+        const int u = units_total <= 0 ? 0 : nu == 0 ? static_cast<int>(blockIdx.x)
+                                                     : static_cast<int>(gridDim.x) + atomicAdd(plan + P_TICKET, 1);
+#else
         const int u = units_total > 0 ? atomicAdd(plan + P_TICKET, 1) : 0;
+#endif
         unsigned long long* ut = (tr && nu < kFfnTraceUnits) ? tr + 8 + 4 * nu : nullptr;
         if (ut) { ut[0] = u; ut[1] = globaltimer_ns(); }
         const bool done = u >= units_total;
