@@ -183,14 +183,14 @@ __device__ __forceinline__ float4 load_y4(const float* src, int ksplit, size_t s
   return a;
 }
 
-__global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
+__global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
                                                       int d_h, int d_h_pad, const int32_t* __restrict__ plan,
                                                       const int32_t* __restrict__ slot_row,
                                                       const float* __restrict__ w, int T, int K, int n_shared,
                                                       float* __restrict__ y, __nv_bfloat16* __restrict__ y_bf16,
                                                       float* __restrict__ x_res, __nv_bfloat16* __restrict__ h_next,
                                                       float eps) {
-  __shared__ float s_red[8];
+  __shared__ float s_red[16];
   __shared__ int s_row[64];
   __shared__ float s_w[64];
   // slot rows / weights / the plan come from kernels that completed before the FFN started;
@@ -211,15 +211,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
   float ss = 0.f;
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec) {
     // y_perm rows are d_h_pad (multiple of 128) wide, so the 4-float reads never leave the row
-    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    float acc[kRowChunks][4] = {};
     for (int k0 = 0; k0 < nslot; k0 += kCombBatch) {
-      float4 v[kCombBatch][2];
+      float4 v[kCombBatch][kRowChunks];
 #pragma unroll
       for (int b = 0; b < kCombBatch; ++b) {
         const int k = k0 + b;
         const int row = k < nslot ? s_row[k] : -1;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < kRowChunks; ++c) {
           const int f = row_chunk(base, c);
           v[b][c] = (row >= 0 && f < d_h_pad)
                         ? load_y4(y_perm + static_cast<size_t>(row) * d_h_pad + f, ksplit, split_stride)
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
         const int k = k0 + b;
         if (k >= nslot || s_row[k] < 0) continue;  // batch padding, or an expert owned by another rank (EP)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < kRowChunks; ++c) {
           float* a = acc[c];
           if (k < K) {  // routed slot: products and sums rounded separately, slot order (moe.py:302-307)
             const float wk = s_w[k];
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
       }
     }
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < kRowChunks; ++c) {
       const int f0 = row_chunk(base, c);
       if (f0 >= d_h) continue;
       const size_t o = static_cast<size_t>(t) * d_h + f0;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
       const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
       if (base == 0) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < kRowChunks; ++c) {
           const int f0 = row_chunk(base, c);
           if (f0 >= d_h) continue;
           const size_t o = static_cast<size_t>(t) * d_h + f0;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* __restrict__ 
         return;
       }
       for (int b2 = 0; b2 < d_h; b2 += blockDim.x * kRowVec)
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < kRowChunks; ++c) {
           const int f0 = row_chunk(b2, c);
           for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
             const size_t o = static_cast<size_t>(t) * d_h + f0 + q;

@@ -395,15 +395,15 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
 // x += y (if y), h = bf16(x * rsqrt(mean(x^2) + eps)); one CTA per token with the
 // traversal and reduction tree of the combine kernel's fused epilogue (rowops.cuh), so
 // the unfused expert-parallel step reproduces the fused single-GPU step bit for bit.
-__global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
+__global__ void __launch_bounds__(kRowMaxThreads) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ y,
                                                                __nv_bfloat16* __restrict__ h, int d_h, float eps) {
-  __shared__ float s_red[8];
+  __shared__ float s_red[16];
   pdl_wait();
   pdl_trigger();
   const int t = blockIdx.x;
   float ss = 0.f;
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec)
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < kRowChunks; ++c) {
       const int f0 = row_chunk(base, c);
       for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
         const size_t o = static_cast<size_t>(t) * d_h + f0 + q;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
   const float tot = block_sum(ss, s_red);
   const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec)
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < kRowChunks; ++c) {
       const int f0 = row_chunk(base, c);
       for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
         const size_t o = static_cast<size_t>(t) * d_h + f0 + q;

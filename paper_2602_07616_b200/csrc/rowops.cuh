@@ -11,11 +11,16 @@
 
 namespace sere {
 
-constexpr int kRowVec = 8;
+#ifndef SERE_ROW_CHUNKS
+#define SERE_ROW_CHUNKS 2
+#endif
+constexpr int kRowChunks = SERE_ROW_CHUNKS;  // 4-element chunks per thread per row block
+constexpr int kRowVec = 4 * kRowChunks;
+constexpr int kRowMaxThreads = 512;
 
 __host__ __device__ inline int row_threads(int d_h) {
   int t = ((d_h + kRowVec - 1) / kRowVec + 31) / 32 * 32;
-  return t < 32 ? 32 : (t > 256 ? 256 : t);
+  return t < 32 ? 32 : (t > kRowMaxThreads ? kRowMaxThreads : t);
 }
 
 // element offset of chunk c (0/1) of thread tid in the row block starting at `base`
@@ -29,7 +34,7 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst, const float (&v
   *reinterpret_cast<uint2*>(dst) = u;
 }
 
-// sum over the block (warp xor tree, then warps in index order); s_red >= 8 floats
+// sum over the block (warp xor tree, then warps in index order); s_red >= 16 floats
 __device__ __forceinline__ float block_sum(float v, float* s_red) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
