@@ -77,7 +77,7 @@ class ExpertBank:
         self.M, self.n_shared, self.d_h, self.d_m = int(n_experts), int(n_shared), int(d_h), int(d_m)
         self.n_total = self.M + self.n_shared
         nbytes = _lib.load().sere_expert_bank_bytes(self.n_total, self.d_h, self.d_m)
-        self.data = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.data = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)  # padding tiles stay 0
 
     @property
     def weight_bytes_per_expert(self) -> int:
@@ -393,6 +393,8 @@ def bank_for(layer: Any) -> ExpertBank:
     """ExpertBank of a reference MoELayer, converted once and cached by identity."""
     if isinstance(layer, ExpertBank):
         return layer
+    if isinstance(getattr(layer, "bank", None), ExpertBank):  # io.GpuLayer
+        return layer.bank
     hit = _BANKS.get(id(layer))
     if hit is not None and hit[0] is layer:
         return hit[1]
@@ -501,8 +503,10 @@ def model_forward(model: Any, batch: Any, config: Any = None, sims: Sequence | N
             wts = torch.as_tensor(np.asarray(a.weights, dtype=np.float32)).to(dev)
             original = a
         else:
-            wr = torch.as_tensor(np.asarray(layer.router.w_router, dtype=np.float32)).to(dev)
-            ids, wts = route_topk_device(router_weight_t(wr), x, int(layer.router.top_k))
+            wr = layer.router.w_router
+            if not isinstance(wr, torch.Tensor):
+                wr = torch.as_tensor(np.asarray(wr, dtype=np.float32))
+            ids, wts = route_topk_device(router_weight_t(wr.to(dev)), x, int(layer.router.top_k))
             original = Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
         if apply_rewrite:
             dsim = _rr._cached_sim(sims[l], dev)
