@@ -304,15 +304,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           if (!(p.dbg_mode & 1)) {
             if (U.dn) {  // k-tile kk: the unit's 1-2 adjacent m-tiles, one copy (pages kk-major)
               for (int kk = 0; kk < nk; ++kk) {
-#if SERE_W2_PAIRS
-                bulk_g2s(pg + (bp + kk * U.mwu) * kPageBytes, a_unit + static_cast<size_t>(kt + kk) * 2 * kTileBytes,
-                         U.mwu * kTileBytes, &tail->full[e], pol_w);
-#else
-                for (int j = 0; j < U.mwu; ++j)
-                  bulk_g2s(pg + (bp + kk * U.mwu + j) * kPageBytes,
-                           p.w2 + w2_tile_offset(U.expert, U.mt0 + j, kt + kk, p.tiles_dn, p.ktiles_dn), kTileBytes,
-                           &tail->full[e], pol_w);
-#endif
+                bulk_g2s(pg + (bp + kk * U.mwu) * kPageBytes,
+                         a_unit + static_cast<size_t>(kt + kk) * kW2Group * kTileBytes, U.mwu * kTileBytes,
+                         &tail->full[e], pol_w);
               }
             } else {  // feature block j at k-tiles kt..kt+nk-1: gate/up tiles, one contiguous copy
               const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;

@@ -133,26 +133,22 @@ inline Dims make_dims(int d_h, int d_m) {
 }
 
 // bank layout: W13 tiles [Et][tiles_gu][ktiles_gu][gate, up] then W2 tiles
-// [Et][ceil(tiles_dn/2)][ktiles_dn][2]: the two m-tiles of a down unit are adjacent at every
-// k-tile, so one 32 KB copy feeds both accumulators
+// [Et][ceil(tiles_dn/G)][ktiles_dn][G] (G = kW2Group): the m-tiles of a down unit are
+// adjacent at every k-tile, so one copy feeds all its accumulators
 inline size_t bank_w13_bytes(int Et, const Dims& d) {
   return static_cast<size_t>(Et) * d.tiles_gu * d.ktiles_gu * 2 * kTileBytes;
 }
-#ifndef SERE_W2_PAIRS
-#define SERE_W2_PAIRS 1
-#endif
+// down tiles are stored in groups of kW2Group m-tiles that sit side by side at every
+// k-tile (a down unit of up to kW2Group m-tiles reads one contiguous run per k-step)
+constexpr int kW2Group = kMwDnMax;
 inline size_t bank_w2_bytes(int Et, const Dims& d) {
-  return static_cast<size_t>(Et) * ((d.tiles_dn + 1) / 2) * 2 * d.ktiles_dn * kTileBytes;
+  return static_cast<size_t>(Et) * ((d.tiles_dn + kW2Group - 1) / kW2Group) * kW2Group * d.ktiles_dn * kTileBytes;
 }
 // byte offset of down tile (expert e, m-tile mt, k-tile kt) inside the W2 region
-static_assert(!SERE_W2_PAIRS || SERE_MW_DN_MAX <= 2, "paired W2 tiles feed down units of at most 2 m-tiles");
 __host__ __device__ inline size_t w2_tile_offset(int e, int mt, int kt, int tiles_dn, int ktiles_dn) {
-#if SERE_W2_PAIRS
-  return ((static_cast<size_t>(e) * ((tiles_dn + 1) / 2) + (mt >> 1)) * ktiles_dn + kt) * 2 * kTileBytes +
-         static_cast<size_t>(mt & 1) * kTileBytes;
-#else
-  return ((static_cast<size_t>(e) * tiles_dn + mt) * ktiles_dn + kt) * static_cast<size_t>(kTileBytes);
-#endif
+  const int groups = (tiles_dn + kW2Group - 1) / kW2Group;
+  return ((static_cast<size_t>(e) * groups + mt / kW2Group) * ktiles_dn + kt) * kW2Group * kTileBytes +
+         static_cast<size_t>(mt % kW2Group) * kTileBytes;
 }
 
 }  // namespace sere
