@@ -63,6 +63,9 @@ constexpr int kEpiWarps = SERE_EPI_WARPS;   // epilogue warps: kEpiWarps/4 per T
 constexpr int kEpiGroups = kEpiWarps / 4;   // warp groups splitting a unit's 16-column chunks
 constexpr int kFfnThreads = 64 + 32 * kEpiWarps;
 constexpr int kPdlPrefetch = 4;
+#ifndef SERE_DEP_DEFER
+#define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
+#endif
 #ifndef SERE_STATIC_FIRST
 #define SERE_STATIC_FIRST 1
 #endif  // k-steps whose weights are issued before waiting on the permute kernel
@@ -211,12 +214,23 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       unsigned long long w_empty = 0, w_dep = 0, w_q = 0, w_empty_dn = 0;
       // PDL: weights do not depend on the preceding kernel (permute), so the first k-steps'
       // weight tiles are issued before griddepcontrol.wait; their activation tiles follow it
+      // The same deferral serves a down unit whose group's h is not complete yet: its weight
+      // tiles stream while the gate/up units of the group finish, and its h tiles follow
+      // the dependency wait. "gates" = PDL not yet waited / dependency not yet met.
       bool pdl_done = false;
+      int dep_g = -1, dep_need = 0;  // open dependency gate of the current down unit
       int n_pend = 0;
       uint32_t pend_dst[kPdlPrefetch], pend_bytes[kPdlPrefetch], pend_bar[kPdlPrefetch];
       const uint8_t* pend_src[kPdlPrefetch];
       auto pdl_flush = [&]() {
-        pdl_wait();
+        if (!pdl_done) pdl_wait();
+        if (dep_g >= 0) {
+          const long long t0 = tr ? clock64() : 0;
+          while (ld_acquire_gpu(dep + dep_g) < dep_need) __nanosleep(64);
+          if (tr) w_dep += static_cast<unsigned long long>(clock64() - t0);
+          fence_proxy_async_global();  // h was written by generic stores on other SMs
+          dep_g = -1;
+        }
         for (int i = 0; i < n_pend; ++i)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
@@ -253,13 +267,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         size_t a_mt_stride;  // bytes between consecutive m-tiles (feature blocks) of the expert
         uint32_t a_copy;     // bytes of one m-tile at one k-step (gate+up adjacent for gate/up)
         if (U.dn) {
-          // h of this group must be complete: every gate/up unit of the group published it
+          // h of this group must be complete (every gate/up unit of the group published it)
+          // before its h tiles are copied; if not yet, the gate defers them (pdl_flush)
           if (ld_acquire_gpu(dep + U.g) < U.need) {
-            const long long t0 = tr ? clock64() : 0;
-            while (ld_acquire_gpu(dep + U.g) < U.need) __nanosleep(64);
-            if (tr) w_dep += static_cast<unsigned long long>(clock64() - t0);
+            dep_g = U.g;
+            dep_need = U.need;
+            if (!SERE_DEP_DEFER) pdl_flush();  // experiment switch: wait before the weights too
+          } else {
+            fence_proxy_async_global();
           }
-          fence_proxy_async_global();
           a_copy = kTileBytes;
           a_mt_stride = 0;  // unused: the unit's m-tiles are adjacent per k-tile (w2_tile_offset)
           a_unit = p.w2 + w2_tile_offset(U.expert, U.mt0, 0, p.tiles_dn, p.ktiles_dn);
@@ -291,7 +307,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
               busy = ranges_overlap(head, np, tail->e_page[s2 % kEntries], tail->e_np[s2 % kEntries]);
             if (!busy) break;
             // an in-flight k-step can only complete once its deferred activation copy is issued
-            if (!pdl_done) pdl_flush();
+            if (!pdl_done || dep_g >= 0) pdl_flush();
             mbar_wait_timed(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u,
                             acc_empty ? (U.dn ? &w_empty_dn : acc_empty) : nullptr);
             ++oldest;
@@ -315,11 +331,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
                          &tail->full[e], pol_w);
             }
           }
-          if (!pdl_done && (U.dn || n_pend + nk > kPdlPrefetch)) pdl_flush();
+          const bool gated = !pdl_done || dep_g >= 0;
+          if (gated && n_pend + nk > kPdlPrefetch) pdl_flush();
           for (int kk = 0; kk < nk; ++kk) {
             uint8_t* bdst = pg + kk * bpk * kPageBytes;
             const uint8_t* bsrc = b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128;
-            if (pdl_done) {
+            if (pdl_done && dep_g < 0) {
               bulk_g2s(bdst, bsrc, b_bytes, &tail->full[e], pol_x);
             } else {
               pend_dst[n_pend] = smem_u32(bdst);
@@ -331,7 +348,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           }
           head += np;
         }
-        if (!pdl_done) pdl_flush();
+        if (!pdl_done || dep_g >= 0) pdl_flush();
         if (ut) ut[3] = globaltimer_ns();
       }
       if (!pdl_done) pdl_flush();
