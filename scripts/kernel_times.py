@@ -16,7 +16,7 @@ def main():
     ap.add_argument("--mode", default="sere")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--T", type=int, default=512)
-    ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--pdl", type=int, default=0)
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
