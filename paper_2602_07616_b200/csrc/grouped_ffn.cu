@@ -61,7 +61,15 @@ constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
 #endif
 constexpr int kEpiWarps = SERE_EPI_WARPS;   // epilogue warps: kEpiWarps/4 per TMEM lane quadrant
 constexpr int kEpiGroups = kEpiWarps / 4;   // warp groups splitting a unit's 16-column chunks
-constexpr int kFfnThreads = 64 + 32 * kEpiWarps;
+#ifndef SERE_MMA_WARPS
+#define SERE_MMA_WARPS 2
+#endif
+// MMA issuer warps (one lane each), splitting a unit's accumulators: tcgen05.mma issue is
+// latency-bound per issuing thread (scripts/micro/mma_rate.cu: 87 -> 59 cycles/MMA at
+// N = 96 with two issuers), so two issuers interleave their issue chains
+constexpr int kMmaWarps = SERE_MMA_WARPS;
+constexpr int kEpiWarp0 = 1 + kMmaWarps;
+constexpr int kFfnThreads = 32 * (1 + kMmaWarps + kEpiWarps);
 constexpr int kPdlPrefetch = 4;
 #ifndef SERE_DEP_DEFER
 #define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
@@ -84,7 +92,7 @@ struct __align__(16) FfnSmemTail {
   uint64_t q_empty[kQueue];
   int32_t queue[kQueue];
   int32_t e_page[kEntries], e_np[kEntries];  // producer: pages held by in-flight k-steps
-  int32_t t_col[kTq], t_need[kTq];           // MMA: TMEM columns held by in-flight units
+  int32_t t_col[kMmaWarps][kTq], t_need[kMmaWarps][kTq];  // MMA: TMEM columns of in-flight units
   uint32_t tmem_base;
   int32_t n_groups, units_gu, units_dn;
 };
@@ -173,9 +181,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   const int ng = status == 0 ? plan[P_NGROUPS] : 0;
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < kEntries; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], 1); }
-    for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], 1); mbar_init(&tail->tempty[i], kEpiWarps); }
-    for (int i = 0; i < kQueue; ++i) { mbar_init(&tail->q_full[i], 1); mbar_init(&tail->q_empty[i], 1 + kEpiWarps); }
+    for (int i = 0; i < kEntries; ++i) { mbar_init(&tail->full[i], 1); mbar_init(&tail->empty[i], kMmaWarps); }
+    for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], kMmaWarps); mbar_init(&tail->tempty[i], kEpiWarps); }
+    for (int i = 0; i < kQueue; ++i) {
+      mbar_init(&tail->q_full[i], 1);
+      mbar_init(&tail->q_empty[i], kMmaWarps + kEpiWarps);
+    }
     fence_mbar_init();
     tail->n_groups = ng;
     tail->units_gu = status == 0 ? plan[P_UNITS_GU] : 0;
@@ -353,13 +364,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       }
       if (!pdl_done) pdl_flush();
     }
-  } else if (warp == 1) {
+  } else if (warp < kEpiWarp0) {
     if (lane == 0) {
-      // ===================== MMA issuer (single thread)
+      // ===================== MMA issuers: issuer mi takes the unit's accumulators a with
+      // a % kMmaWarps == mi; both walk every k-step (full/empty barriers count both)
+      const int mi = warp - 1;
       int qs = 0, iter = 0, head = 0, kstep = 0, tcol = 0, oldest = 0;
       uint32_t qph = 0;
       unsigned long long w_full = 0, w_tmem = 0, nks = 0, w_full_dn = 0, w_tmem_dn = 0, nks_dn = 0;
-      unsigned long long* acc_full = tr ? &w_full : nullptr;
+      unsigned long long* acc_full = (tr && mi == 0) ? &w_full : nullptr;
+      if (mi != 0) tr = nullptr;  // issuer 0 keeps the trace
       for (;; ++iter) {
         mbar_wait(&tail->q_full[qs], qph);
         const int u = tail->queue[qs];
@@ -382,14 +396,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         for (;;) {  // release in FIFO order until no in-flight unit holds these columns
           bool busy = iter - oldest >= kTq;
           for (int i2 = oldest; !busy && i2 < iter; ++i2)
-            busy = ranges_overlap(col, need, tail->t_col[i2 % kTq], tail->t_need[i2 % kTq]);
+            busy = ranges_overlap(col, need, tail->t_col[mi][i2 % kTq], tail->t_need[mi][i2 % kTq]);
           if (!busy) break;
           mbar_wait_timed(&tail->tempty[oldest % kTq], static_cast<uint32_t>(oldest / kTq) & 1u,
                           tr ? (U.dn ? &w_tmem_dn : &w_tmem) : nullptr);
           ++oldest;
         }
-        tail->t_col[iter % kTq] = col;
-        tail->t_need[iter % kTq] = need;
+        tail->t_col[mi][iter % kTq] = col;
+        tail->t_need[mi][iter % kTq] = need;
         tc_fence_after();
         const int bpk = ktile_bpages(U), apj = U.dn ? 1 : 2;  // A tiles per m-tile block and k-tile
         const uint32_t idesc = umma_idesc_bf16(128, U.n_mma);
@@ -409,6 +423,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
               const uint32_t b_addr = pg_addr + kk * bpk * kPageBytes;
               for (int j = 0; j < U.mwu; ++j) {
                 for (int s2 = 0; s2 < apj; ++s2) {  // accumulator j*apj + s2 (gate/up: gate then up)
+                  if ((j * apj + s2) % kMmaWarps != mi) continue;
                   const int apage = U.dn ? bp + kk * U.mwu + j : bp + (j * nk + kk) * apj + s2;
                   const uint32_t a_addr = pg_addr + apage * kPageBytes;
                   const uint32_t dj = d0 + (j * apj + s2) * U.n_mma;
@@ -429,9 +444,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       }
     }
   } else {
-    // ===================== epilogue warps 2..5 -> TMEM lane quadrant q = warp % 4
-    const int q = warp & 3;               // TMEM lane quadrant of this warp
-    const int eg = (warp - 2) / 4;         // column group: chunks c0 = 16 * (eg + kEpiGroups * i)
+    // ===================== epilogue warps -> TMEM lane quadrant q = warp % 4
+    const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    const int eg = (warp - kEpiWarp0) / 4;     // column group: chunks c0 = 16 * (eg + kEpiGroups * i)
     int qs = 0, iter = 0, tcol = 0;
     uint32_t qph = 0;
     unsigned long long w_tf = 0;
@@ -442,7 +457,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       if (lane == 0) mbar_arrive(&tail->q_empty[qs]);
       if (++qs == kQueue) { qs = 0; qph ^= 1u; }
       if (u < 0) {
-        if (tr && warp == 2 && lane == 0) tr[6] = w_tf;
+        if (tr && warp == kEpiWarp0 && lane == 0) tr[6] = w_tf;
         break;
       }
       const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       const int col = tcol;
       tcol += need;
       mbar_wait_timed(&tail->tfull[iter % kTq], static_cast<uint32_t>(iter / kTq) & 1u,
-                      (tr && warp == 2 && lane == 0) ? &w_tf : nullptr);
+                      (tr && warp == kEpiWarp0 && lane == 0) ? &w_tf : nullptr);
       __syncwarp();
       tc_fence_after();
       const uint32_t tq = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col;
@@ -499,13 +514,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tail->tempty[iter % kTq]);
-      if (tr && warp == 2 && lane == 0 && iter < kFfnTraceUnits) tr[816 + iter] = globaltimer_ns();
+      if (tr && warp == kEpiWarp0 && lane == 0 && iter < kFfnTraceUnits) tr[816 + iter] = globaltimer_ns();
       if (!U.dn) {
         // publish this unit's slice of h: the down units of the group (any SM) read it with
         // bulk copies (async proxy) after acquiring the counter
         fence_proxy_async_global();
         named_bar_sync(1, 32 * kEpiWarps);
-        if (warp == 2 && lane == 0) {
+        if (warp == kEpiWarp0 && lane == 0) {
           __threadfence();
           atomicAdd(dep + U.g, 1);
         }

@@ -111,6 +111,42 @@ __global__ void __launch_bounds__(128, 1) mma_order(int n, int iters, int mw, lo
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
+__global__ void __launch_bounds__(128, 1) mma_two_issuers(int n, int iters, int mw, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if ((warp == 1 || warp == 2) && lane == 0) {
+    const int w = warp - 1;
+    const uint32_t idesc = umma_idesc_bf16(128, n);
+    const uint32_t b_addr = smem_u32(smem);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int j = 0; j < mw; ++j) {
+        const uint32_t a_addr = b_addr + 32768 + (w * mw + j) * 16384;
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(tbase + (w * mw + j) * n, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k),
+                    idesc, (it > 0 || k > 0) ? 1u : 0u);
+      }
+      umma_commit(&bar[w]);
+    }
+    mbar_wait(&bar[w], (iters - 1) & 1);
+    long long t2 = clock64();
+    if (w == 0) out[blockIdx.x * 2 + 1] = t2 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
 __global__ void __launch_bounds__(128, 1) mma_rate(int n, int iters, int mw, long long* out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -152,6 +188,7 @@ int main() {
   long long* d;
   cudaMalloc(&d, 2 * 148 * sizeof(long long));
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(mma_two_issuers, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   int ns[] = {16, 32, 64, 96, 128, 192, 256};
   for (int mw : {1, 2, 4}) {
     for (int n : ns) {
@@ -187,8 +224,15 @@ int main() {
         cudaMemcpy(h3, d, sizeof(h3), cudaMemcpyDeviceToHost);
         q[1] = double(h3[1]) / (iters * mw * 4);
       }
-      printf("mw=%d N=%3d: j-major %.1f | k-major %.1f | 2-acc %.1f cyc/mma (floor %.1f)\n", mw, n, r[0], q[0], q[1],
-             128.0 * n / 256.0);
+      double two = 0;
+      if (2 * mw * n <= 512 && 2 * mw <= 8) {
+        mma_two_issuers<<<148, 128, 200 * 1024>>>(n, iters, mw, d);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h3, d, sizeof(h3), cudaMemcpyDeviceToHost);
+        two = double(h3[1]) / (iters * mw * 4 * 2);
+      }
+      printf("mw=%d N=%3d: j-major %.1f | k-major %.1f | 2-acc %.1f | 2 issuers %.1f cyc/mma (floor %.1f)\n", mw, n,
+             r[0], q[0], q[1], two, 128.0 * n / 256.0);
     }
   }
   return 0;
