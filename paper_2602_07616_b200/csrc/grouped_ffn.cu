@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           head += np;
         }
         umma_commit(&tail->tfull[iter % kTq]);
+        if (tr && iter < kFfnTraceUnits) tr[1280 + iter] = globaltimer_ns();  // last MMA issued
       }
     }
   } else {
@@ -467,46 +468,71 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       tcol += need;
       mbar_wait_timed(&tail->tfull[iter % kTq], static_cast<uint32_t>(iter / kTq) & 1u,
                       (tr && warp == kEpiWarp0 && lane == 0) ? &w_tf : nullptr);
+      if (tr && warp == kEpiWarp0 && lane == 0 && iter < kFfnTraceUnits) tr[1024 + iter] = globaltimer_ns();
       __syncwarp();
       tc_fence_after();
       const uint32_t tq = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col;
+      // The epilogue is issue-bound (one store per element per thread): addresses are
+      // strength-reduced per 16-row chunk. Unit rows start on a 16-row boundary
+      // (kRowAlign) and chunks are 16 rows, so the swizzle phase of row c0 + i is i & 7.
       if (!U.dn) {
         // feature f of block fb: its gate and up accumulators sit in this thread's TMEM lane,
         // so h = act(g) * u needs no data exchange; one bf16 per (row, f) into the swizzled
         // B layout of the down phase
         for (int j = 0; j < U.mwu; ++j) {
           const int f = (U.mt0 + j) * 128 + q * 32 + lane;
-          const int fl = f & 63;
-          uint8_t* hbase = p.h_pack + static_cast<size_t>(f >> 6) * p.r_max * 128 + (fl & 7) * 2;
+          const int fl = f & 63, ch = fl >> 3;
+          uint8_t* hcol = p.h_pack + static_cast<size_t>(f >> 6) * p.r_max * 128 +
+                          static_cast<size_t>(U.row0) * 128 + (fl & 7) * 2;
           const uint32_t tg = tq + (2 * j) * U.n_mma, tu = tg + U.n_mma;
           for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
             uint32_t rg[16], ru[16];
             tmem_ld16(tg + c0, rg);
             tmem_ld16(tu + c0, ru);
             tmem_wait_ld();
+            float hv[16];
+            if (p.act == 0) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int row = U.row0 + c0 + i;
-              const float h = act_apply(__uint_as_float(rg[i]), p.act) * __uint_as_float(ru[i]);
-              *reinterpret_cast<__nv_bfloat16*>(hbase + static_cast<size_t>(row) * 128 +
-                                                sw128_chunk(fl >> 3, row) * 16) = __float2bfloat16_rn(h);
+              for (int i = 0; i < 16; ++i) {
+                const float g = __uint_as_float(rg[i]);
+                hv[i] = __fdividef(g, 1.0f + __expf(-g)) * __uint_as_float(ru[i]);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) hv[i] = act_apply(__uint_as_float(rg[i]), p.act) * __uint_as_float(ru[i]);
             }
+            uint8_t* hp = hcol + static_cast<size_t>(c0) * 128;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              *reinterpret_cast<__nv_bfloat16*>(hp + i * 128 + ((ch ^ (i & 7)) << 4)) = __float2bfloat16_rn(hv[i]);
           }
         }
       } else {
-        for (int j = 0; j < U.mwu; ++j) {
-          const int feat = (U.mt0 + j) * 128 + q * 32 + lane;
-          float* ybase = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * p.d_h_pad;
-          const uint32_t taddr = tq + j * U.n_mma;
-          for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
-            uint32_t r[16];
-            tmem_ld16(taddr + c0, r);
-            tmem_wait_ld();
+        // down: both m-tiles' chunk loads in flight behind one wait; fp32 rows of y_perm
+        const size_t ld = p.d_h_pad;
+        float* ycol = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * ld + static_cast<size_t>(U.row0) * ld +
+                      U.mt0 * 128 + q * 32 + lane;
+        const bool store = !(p.dbg_mode & 4);
+        for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
+          uint32_t r[kMwDnMax][16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int jr = c0 + i;
-              if (jr < U.rows_valid && !(p.dbg_mode & 4))
-                ybase[static_cast<size_t>(U.row0 + jr) * p.d_h_pad + feat] = __uint_as_float(r[i]);
+          for (int j = 0; j < kMwDnMax; ++j)
+            if (j < U.mwu) tmem_ld16(tq + j * U.n_mma + c0, r[j]);
+          tmem_wait_ld();
+          const int nv = U.rows_valid - c0;
+          if (store) {
+#pragma unroll
+            for (int j = 0; j < kMwDnMax; ++j) {
+              if (j < U.mwu) {
+                float* yp = ycol + static_cast<size_t>(c0) * ld + j * 128;
+                if (nv >= 16) {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) { *yp = __uint_as_float(r[j][i]); yp += ld; }
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) { if (i < nv) *yp = __uint_as_float(r[j][i]); yp += ld; }
+                }
+              }
             }
           }
         }

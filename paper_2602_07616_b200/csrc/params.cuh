@@ -50,7 +50,7 @@ struct FfnParams {
                               // bit2 skip the expert-output stores
   unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
 };
-constexpr int kFfnTraceStride = 1024;
+constexpr int kFfnTraceStride = 2048;
 constexpr int kFfnTraceUnits = 200;
 
 extern long long* g_route_dbg;

@@ -38,7 +38,7 @@ def main() -> None:
     torch.cuda.synchronize()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     traces = []
-    bufs = [torch.zeros(sms * 1024, dtype=torch.int64, device="cuda") for _ in range(a.layers)]
+    bufs = [torch.zeros(sms * 2048, dtype=torch.int64, device="cuda") for _ in range(a.layers)]
 
     def hook(i):  # eager step: point the kernel at layer i's trace buffer before its launch
         lib.sere_debug_set_ffn_trace(bufs[i].data_ptr())
@@ -52,7 +52,7 @@ def main() -> None:
     acts = step.active_counts()
     unit_bytes = {}  # filled per layer below (weights per unit from the plan is not exported: approximate)
     for l in range(a.layers):
-        tr = bufs[l].view(sms, 1024).cpu().numpy().astype(np.int64)
+        tr = bufs[l].view(sms, 2048).cpu().numpy().astype(np.int64)
         if tr[:, 0].max() == 0:
             continue
         t0 = tr[:, 0].min()
