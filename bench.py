@@ -89,8 +89,14 @@ def measured_peak_hbm():
 
 def ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of moe_ffn_kernel from the committed
-    `ncu --set full` capture (newest profiles/r*_ncu_traffic.json), per launch."""
-    files = sorted(ROOT.glob("profiles/r*_ncu_traffic.json"))
+    `ncu --set full` capture (newest profiles/r*_ncu_traffic*.json by round and capture version), per launch."""
+    import re
+
+    def version(f):  # r01_ncu_traffic.json < r01_ncu_traffic_v5.json < ... (round, then capture version)
+        m = re.match(r"r(\d+)_ncu_traffic(?:_v(\d+))?\.json$", f.name)
+        return (int(m.group(1)), int(m.group(2) or 0)) if m else (-1, -1)
+
+    files = sorted(ROOT.glob("profiles/r*_ncu_traffic*.json"), key=version)
     if not files:
         return None, None
     try:
