@@ -223,6 +223,64 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
                           void* workspace, size_t workspace_bytes, int reps, void* stream);
 
 /* ------------------------------------------------------------------------
+ * (4c) Expert parallel over NVLink peer memory (replaces the NCCL
+ *     all-gather / reduce-scatter choreography of (4b) -- the reference has no
+ *     multi-GPU path, so these have no reference counterpart beyond moe.py:280-310).
+ *     Each rank owns: gathered token states h_all bf16 [T_all,d_h], router ids_all
+ *     i32 [T_all,K] and w_all f32 [T_all,K], barrier flags i32 [world] (zeroed once),
+ *     and its layer workspace (y_perm / slot_row inside it, sere_layer_workspace_layout).
+ *     All of them must be reachable from every rank (cudaIpcOpenMemHandle, see
+ *     sere_ipc_*); sere_ep_peers lists every rank's pointers, entry `rank` = own.
+ *     Per layer:  sere_route_topk_ep -> sere_ep_barrier -> sere_moe_ffn_ep ->
+ *                 sere_ep_barrier -> sere_combine_ep.
+ * ------------------------------------------------------------------------ */
+#define SERE_MAX_EP_RANKS 8
+typedef struct {
+  int32_t world, rank;
+  int32_t t0, T_all;                      /* this rank's first token; tokens of the batch       */
+  int32_t e_lo[SERE_MAX_EP_RANKS + 1];    /* rank r owns routed experts [e_lo[r], e_lo[r+1])    */
+  int32_t nsh[SERE_MAX_EP_RANKS];         /* shared experts s with s % world == r                */
+  int32_t r_max[SERE_MAX_EP_RANKS];       /* sere_ws_layout.r_max of rank r's workspace          */
+  const float* y_perm[SERE_MAX_EP_RANKS]; /* rank r: workspace + off_y_perm                      */
+  const int32_t* slot_row[SERE_MAX_EP_RANKS]; /* rank r: workspace + off_slot_row               */
+  uint16_t* h_all[SERE_MAX_EP_RANKS];
+  int32_t* ids_all[SERE_MAX_EP_RANKS];
+  float* w_all[SERE_MAX_EP_RANKS];
+  int32_t* flags[SERE_MAX_EP_RANKS];
+} sere_ep_peers;
+
+/* Router for this rank's T_local = T_all/world tokens (x_local = own h_all rows
+ * [t0, t0+T_local)); ids/weights rows are stored into EVERY rank's ids_all/w_all. */
+int sere_route_topk_ep(const sere_ep_peers* peers, const uint16_t* x_local, const uint16_t* w_router_t,
+                       const float* bias, int T_local, int d_h, int M, int K, void* workspace,
+                       size_t workspace_bytes, void* stream);
+/* Flag barrier over the group (one warp). epoch_dev: this rank's device counter (zeroed
+ * once). On a wait longer than timeout_ns: SERE_ERR_CUDA in status_dev, no hang. */
+int sere_ep_barrier(const sere_ep_peers* peers, int32_t* epoch_dev, int32_t* status_dev, int64_t timeout_ns,
+                    void* stream);
+/* (4b) without its combine: re-route + align + permute + fused FFN of this rank's experts
+ * over the whole gathered batch; the expert outputs stay in the workspace for the peers. */
+int sere_moe_ffn_ep(const void* bank, int M, int expert_lo, int expert_hi, int n_shared_local, int d_h, int d_m,
+                    int activation, const double* sim, int S, double rho, int flags, const uint16_t* x_all,
+                    const int32_t* ids_all, const float* w_all, int T_all, int K, int32_t* ids_out,
+                    uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
+                    void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream);
+/* Combine of this rank's tokens from the owners' expert outputs (peer loads), fixed slot
+ * order: x_res[t] += y[t]; every rank's h_all row t0+t = bf16(RMSNorm(x_res[t])).
+ * ids_rr = this rank's re-routed ids [T_all,K] (sere_moe_ffn_ep ids_out; identical on
+ * every rank). y_local f32 [T_local,d_h] (nullable) receives y itself. */
+int sere_combine_ep(const sere_ep_peers* peers, const int32_t* ids_rr, const void* workspace, int M_local,
+                    int n_shared_local, int n_shared_total, int d_h, int d_m, int K, float* x_res, float* y_local,
+                    float eps, void* stream);
+/* CUDA IPC helpers: a 64-byte handle of a cudaMalloc'd base pointer (sere_alloc_peer),
+ * opened in another process of the same node. */
+int sere_alloc_peer(size_t bytes, void** out);
+int sere_free_peer(void* ptr);
+int sere_ipc_handle(void* base_ptr, uint8_t out_handle[64]);
+int sere_ipc_open(const uint8_t handle[64], void** out_ptr);
+int sere_ipc_close(void* ptr);
+
+/* ------------------------------------------------------------------------
  * Introspection of the workspace (tests read the count/align plan back).
  * ------------------------------------------------------------------------ */
 typedef struct {

@@ -18,6 +18,29 @@ LIB_PATH = Path(__file__).resolve().parent / "libsere_b200.so"
 _c_int, _c_double, _c_size, _p = ctypes.c_int, ctypes.c_double, ctypes.c_size_t, ctypes.c_void_p
 
 
+MAX_EP_RANKS = 8
+
+
+class EpPeers(ctypes.Structure):
+    """`sere_ep_peers` of include/sere_b200.h: every rank's peer-reachable pointers."""
+
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("t0", ctypes.c_int32),
+        ("T_all", ctypes.c_int32),
+        ("e_lo", ctypes.c_int32 * (MAX_EP_RANKS + 1)),
+        ("nsh", ctypes.c_int32 * MAX_EP_RANKS),
+        ("r_max", ctypes.c_int32 * MAX_EP_RANKS),
+        ("y_perm", ctypes.c_void_p * MAX_EP_RANKS),
+        ("slot_row", ctypes.c_void_p * MAX_EP_RANKS),
+        ("h_all", ctypes.c_void_p * MAX_EP_RANKS),
+        ("ids_all", ctypes.c_void_p * MAX_EP_RANKS),
+        ("w_all", ctypes.c_void_p * MAX_EP_RANKS),
+        ("flags", ctypes.c_void_p * MAX_EP_RANKS),
+    ]
+
+
 class WsLayout(ctypes.Structure):
     """`sere_ws_layout` of include/sere_b200.h."""
 
@@ -64,6 +87,19 @@ SIGNATURES = {
     "sere_moe_forward_ep": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int,
                                      _c_double, _c_int, _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p,
                                      _c_size, _p, _p]),
+    "sere_route_topk_ep": (_c_int, [ctypes.POINTER(EpPeers), _p, _p, _p, _c_int, _c_int, _c_int, _c_int, _p,
+                                    _c_size, _p]),
+    "sere_ep_barrier": (_c_int, [ctypes.POINTER(EpPeers), _p, _p, ctypes.c_int64, _p]),
+    "sere_moe_ffn_ep": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int,
+                                 _c_double, _c_int, _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _c_size,
+                                 _p, _p]),
+    "sere_combine_ep": (_c_int, [ctypes.POINTER(EpPeers), _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                 _p, _p, ctypes.c_float, _p]),
+    "sere_alloc_peer": (_c_int, [_c_size, ctypes.POINTER(ctypes.c_void_p)]),
+    "sere_free_peer": (_c_int, [_p]),
+    "sere_ipc_handle": (_c_int, [_p, ctypes.c_char * 64]),
+    "sere_ipc_open": (_c_int, [ctypes.c_char * 64, ctypes.POINTER(ctypes.c_void_p)]),
+    "sere_ipc_close": (_c_int, [_p]),
     "sere_route_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
     "sere_route_topk": (_c_int, [_p, _p, _p, _c_int, _c_int, _c_int, _c_int, _p, _p, _p, _p, _c_size, _p]),
     "sere_residual_rmsnorm": (_c_int, [_p, _p, _p, _c_int, _c_int, ctypes.c_float, _p]),

@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsere_b200.so"
-SOURCES = ["capi.cu", "reroute_align.cu", "layout.cu", "grouped_ffn.cu", "router.cu"]
+SOURCES = ["capi.cu", "reroute_align.cu", "layout.cu", "grouped_ffn.cu", "router.cu", "ep_p2p.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -139,12 +139,12 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
               int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
               int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
               int32_t* status_dev, cudaStream_t stream, float* x_res = nullptr, uint16_t* h_next = nullptr,
-              float eps = 0.f) {
+              float eps = 0.f, bool do_combine = true) {
   const WsLayout L = ws_layout(T, K, m_local, n_shared, d_h, d_m);
   if (workspace == nullptr || workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
   if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr)
     return SERE_ERR_DIMENSION;
-  if (y == nullptr && (x_res == nullptr || h_next == nullptr)) return SERE_ERR_DIMENSION;
+  if (do_combine && y == nullptr && (x_res == nullptr || h_next == nullptr)) return SERE_ERR_DIMENSION;
   uint8_t* ws = reinterpret_cast<uint8_t*>(align_up(reinterpret_cast<uintptr_t>(workspace), 1024));
   int32_t* plan = reinterpret_cast<int32_t*>(ws + L.plan);
   int32_t* slot_row = reinterpret_cast<int32_t*>(ws + L.slot_row);
@@ -191,6 +191,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
   stage_mark(3, stream);  // gate/up and down run in one launch: stage 3 is empty
+  if (!do_combine) return SERE_OK;  // expert parallel over peer memory: sere_combine_ep
 
   stage_mark(4, stream);
   e = launch_combine(y_perm, d, L.r_max, plan, slot_row, weights, T, K, n_shared, y,
@@ -387,6 +388,113 @@ int sere_moe_forward_ep(const void* bank, int M, int expert_lo, int expert_hi, i
                    active_list, n_active, y_partial, nullptr, workspace, workspace_bytes, status_dev,
                    static_cast<cudaStream_t>(stream));
 }
+
+// ---------------------------------------------------------------- expert parallel, peer memory
+static_assert(sizeof(sere_ep_peers) == sizeof(EpPeers), "sere_ep_peers must mirror EpPeers");
+static_assert(offsetof(sere_ep_peers, flags) == offsetof(EpPeers, flags), "sere_ep_peers must mirror EpPeers");
+static_assert(SERE_MAX_EP_RANKS == kMaxEpRanks, "rank limit");
+
+static int ep_peers(const sere_ep_peers* in, EpPeers* out) {
+  if (in == nullptr || in->world < 1 || in->world > kMaxEpRanks || in->rank < 0 || in->rank >= in->world)
+    return SERE_ERR_CONFIG;
+  std::memcpy(out, in, sizeof(EpPeers));
+  for (int r = 0; r < in->world; ++r)
+    if (!out->h_all[r] || !out->ids_all[r] || !out->w_all[r] || !out->flags[r]) return SERE_ERR_DIMENSION;
+  return SERE_OK;
+}
+
+int sere_route_topk_ep(const sere_ep_peers* peers, const uint16_t* x_local, const uint16_t* w_router_t,
+                       const float* bias, int T_local, int d_h, int M, int K, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  EpPeers ep;
+  int rc = ep_peers(peers, &ep);
+  if (rc != SERE_OK) return rc;
+  if (T_local < 0 || d_h < 1 || M < 1 || K < 1) return SERE_ERR_DIMENSION;
+  if (K > M) return SERE_ERR_CONFIG;
+  if (ep.t0 < 0 || ep.t0 + T_local > ep.T_all) return SERE_ERR_DIMENSION;
+  if (!route_fast_path(M, K, d_h) || M > kMaxExperts) return SERE_ERR_UNSUPPORTED;
+  if (T_local == 0) return SERE_OK;
+  if (!x_local || !w_router_t) return SERE_ERR_DIMENSION;
+  if (workspace == nullptr || workspace_bytes < route_workspace_bytes(T_local, d_h, M)) return SERE_ERR_WORKSPACE;
+  return check_cuda(launch_route_mma(reinterpret_cast<const __nv_bfloat16*>(x_local),
+                                     reinterpret_cast<const __nv_bfloat16*>(w_router_t), bias, T_local, d_h, M, K,
+                                     nullptr, nullptr, nullptr, workspace, static_cast<cudaStream_t>(stream), &ep));
+}
+
+int sere_ep_barrier(const sere_ep_peers* peers, int32_t* epoch_dev, int32_t* status_dev, int64_t timeout_ns,
+                    void* stream) {
+  EpPeers ep;
+  const int rc = ep_peers(peers, &ep);
+  if (rc != SERE_OK) return rc;
+  if (epoch_dev == nullptr || timeout_ns <= 0) return SERE_ERR_DIMENSION;
+  return check_cuda(launch_ep_barrier(ep, epoch_dev, status_dev, timeout_ns, static_cast<cudaStream_t>(stream)));
+}
+
+int sere_moe_ffn_ep(const void* bank, int M, int expert_lo, int expert_hi, int n_shared_local, int d_h, int d_m,
+                    int activation, const double* sim, int S, double rho, int flags, const uint16_t* x_all,
+                    const int32_t* ids_all, const float* w_all, int T_all, int K, int32_t* ids_out,
+                    uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
+                    void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream) {
+  if (expert_lo < 0 || expert_hi > M || expert_hi < expert_lo) return SERE_ERR_DIMENSION;
+  const int m_local = expert_hi - expert_lo;
+  if (m_local + n_shared_local < 1) return SERE_ERR_DIMENSION;
+  int rc = check_layer_shapes(M, n_shared_local, d_h, d_m, activation, T_all, K);
+  if (rc != SERE_OK) return rc;
+  rc = check_reroute_cfg(K, M, S, rho);
+  if (rc != SERE_OK) return rc;
+  if (sim == nullptr || ids_out == nullptr) return SERE_ERR_DIMENSION;
+  if (T_all == 0) return SERE_OK;
+  return run_layer(bank, M, expert_lo, m_local, n_shared_local, d_h, d_m, activation, sim, S, rho, flags,
+                   MODE_REROUTE | MODE_ALIGN, x_all, ids_all, w_all, T_all, K, ids_out, expert_class, reroute_map,
+                   active_list, n_active, nullptr, nullptr, workspace, workspace_bytes, status_dev,
+                   static_cast<cudaStream_t>(stream), nullptr, nullptr, 0.f, /*do_combine=*/false);
+}
+
+int sere_combine_ep(const sere_ep_peers* peers, const int32_t* ids_rr, const void* workspace, int M_local,
+                    int n_shared_local, int n_shared_total, int d_h, int d_m, int K, float* x_res, float* y_local,
+                    float eps, void* stream) {
+  EpPeers ep;
+  int rc = ep_peers(peers, &ep);
+  if (rc != SERE_OK) return rc;
+  if (M_local < 0 || n_shared_local < 0 || n_shared_total < n_shared_local || d_h < 1 || d_m < 1 || K < 1)
+    return SERE_ERR_DIMENSION;
+  if (K + n_shared_total > 64) return SERE_ERR_UNSUPPORTED;
+  for (int r = 0; r < ep.world; ++r)
+    if (!ep.y_perm[r] || !ep.slot_row[r]) return SERE_ERR_DIMENSION;
+  const int T_local = ep.T_all / ep.world;
+  if (T_local * ep.world != ep.T_all || ep.t0 != ep.rank * T_local) return SERE_ERR_DIMENSION;
+  if (T_local == 0) return SERE_OK;
+  if (!ids_rr || !workspace || !x_res) return SERE_ERR_DIMENSION;
+  const WsLayout L = ws_layout(ep.T_all, K, M_local, n_shared_local, d_h, d_m);
+  uint8_t* ws = ws_base(workspace);
+  return check_cuda(launch_combine(reinterpret_cast<const float*>(ws + L.y_perm), L.d, L.r_max,
+                                   reinterpret_cast<const int32_t*>(ws + L.plan),
+                                   reinterpret_cast<const int32_t*>(ws + L.slot_row), ep.w_all[ep.rank], T_local, K,
+                                   n_shared_total, y_local, nullptr, x_res, nullptr, eps,
+                                   static_cast<cudaStream_t>(stream), &ep, ids_rr));
+}
+
+int sere_alloc_peer(size_t bytes, void** out) {
+  if (out == nullptr || bytes == 0) return SERE_ERR_DIMENSION;
+  return check_cuda(cudaMalloc(out, bytes));
+}
+int sere_free_peer(void* ptr) { return check_cuda(cudaFree(ptr)); }
+int sere_ipc_handle(void* base_ptr, uint8_t out_handle[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  if (base_ptr == nullptr || out_handle == nullptr) return SERE_ERR_DIMENSION;
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, base_ptr);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
+  std::memcpy(out_handle, &h, 64);
+  return SERE_OK;
+}
+int sere_ipc_open(const uint8_t handle[64], void** out_ptr) {
+  if (handle == nullptr || out_ptr == nullptr) return SERE_ERR_DIMENSION;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  return check_cuda(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+int sere_ipc_close(void* ptr) { return check_cuda(cudaIpcCloseMemHandle(ptr)); }
 
 size_t sere_route_workspace_bytes(int T, int d_h, int M) {
   if (T < 0 || d_h < 1 || M < 1) return 0;

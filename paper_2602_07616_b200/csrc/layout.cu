@@ -183,26 +183,60 @@ __device__ __forceinline__ float4 load_y4(const float* src, int ksplit, size_t s
   return a;
 }
 
+// Expert-parallel form (ep.world > 0, ep_p2p.cu): CTA t combines this rank's token
+// t0 + t; each slot's expert output row is read from its owner rank's y_perm over NVLink
+// peer memory (the owner's slot_row says which row), in the same slot order and with the
+// same arithmetic as the single-GPU pass, and h_next is stored into every rank's gathered
+// token-state buffer -- the reduce-scatter and the next layer's all-gather of h are this
+// kernel's loads and stores.
+__device__ __forceinline__ int ep_owner(const EpPeers& ep, int e) {
+  int o = 0;
+  while (o + 1 < ep.world && e >= ep.e_lo[o + 1]) ++o;
+  return o;
+}
+
 __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
                                                       int d_h, int d_h_pad, const int32_t* __restrict__ plan,
                                                       const int32_t* __restrict__ slot_row,
                                                       const float* __restrict__ w, int T, int K, int n_shared,
                                                       float* __restrict__ y, __nv_bfloat16* __restrict__ y_bf16,
                                                       float* __restrict__ x_res, __nv_bfloat16* __restrict__ h_next,
-                                                      float eps) {
+                                                      float eps, const EpPeers ep, const int32_t* __restrict__ ids_rr) {
   __shared__ float s_red[16];
-  __shared__ int s_row[64];
+  __shared__ const float* s_src[64];  // slot's expert-output row (nullptr: not evaluated / not owned)
+  __shared__ size_t s_split[64];      // its K-split plane stride
   __shared__ float s_w[64];
   // slot rows / weights / the plan come from kernels that completed before the FFN started;
   // y_perm (FFN) and x_res (RMW) need the predecessor grid: wait after staging the slots
   if (plan[P_STATUS] != 0) { pdl_wait(); return; }
-  const int TK = T * K;
-  const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
   const int t = blockIdx.x;
-  const int nslot = K + n_shared;  // <= 32 + 31
-  for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
-    s_row[k] = k < K ? slot_row[t * K + k] : slot_row[TK + t * n_shared + (k - K)];
-    s_w[k] = k < K ? w[t * K + k] : 1.f;
+  const int nslot = K + n_shared;  // <= 32 + 31 (EP: n_shared = all shared experts of the layer)
+  if (ep.world == 0) {
+    const int TK = T * K;
+    const size_t split_stride = static_cast<size_t>(r_max) * d_h_pad;
+    for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+      const int row = k < K ? slot_row[t * K + k] : slot_row[TK + t * n_shared + (k - K)];
+      s_src[k] = row >= 0 ? y_perm + static_cast<size_t>(row) * d_h_pad : nullptr;
+      s_split[k] = split_stride;
+      s_w[k] = k < K ? w[t * K + k] : 1.f;
+    }
+  } else {
+    const int tg = ep.t0 + t, TK = ep.T_all * K;
+    for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+      int o, idx;
+      if (k < K) {
+        o = ep_owner(ep, ids_rr[tg * K + k]);
+        idx = tg * K + k;
+      } else {
+        const int s = k - K;
+        o = s % ep.world;
+        idx = TK + tg * ep.nsh[o] + s / ep.world;
+      }
+      const int row = ep.slot_row[o][idx];  // peer load (NVLink) unless o == rank
+      s_src[k] = row >= 0 ? ep.y_perm[o] + static_cast<size_t>(row) * d_h_pad : nullptr;
+      s_split[k] = static_cast<size_t>(ep.r_max[o]) * d_h_pad;
+      s_w[k] = k < K ? w[tg * K + k] : 1.f;
+    }
   }
   __syncthreads();
   pdl_wait();
@@ -217,19 +251,18 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
 #pragma unroll
       for (int b = 0; b < kCombBatch; ++b) {
         const int k = k0 + b;
-        const int row = k < nslot ? s_row[k] : -1;
+        const float* src = k < nslot ? s_src[k] : nullptr;
 #pragma unroll
         for (int c = 0; c < kRowChunks; ++c) {
           const int f = row_chunk(base, c);
-          v[b][c] = (row >= 0 && f < d_h_pad)
-                        ? load_y4(y_perm + static_cast<size_t>(row) * d_h_pad + f, ksplit, split_stride)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[b][c] = (src != nullptr && f < d_h_pad) ? load_y4(src + f, ksplit, s_split[k])
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
 #pragma unroll
       for (int b = 0; b < kCombBatch; ++b) {
         const int k = k0 + b;
-        if (k >= nslot || s_row[k] < 0) continue;  // batch padding, or an expert owned by another rank (EP)
+        if (k >= nslot || s_src[k] == nullptr) continue;  // batch padding, or an expert owned by another rank (EP)
 #pragma unroll
         for (int c = 0; c < kRowChunks; ++c) {
           float* a = acc[c];
@@ -271,19 +304,24 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
         }
       }
     }
-    if (x_res && h_next && base + static_cast<int>(blockDim.x) * kRowVec >= d_h) {
-      // single-block rows (d_h <= 8 * nthreads, the common case): normalise from registers
+    if (x_res && (h_next || ep.world) && base + static_cast<int>(blockDim.x) * kRowVec >= d_h) {
+      // single-block rows (d_h <= 8 * nthreads, the common case): normalise from registers.
+      // Destinations: h_next row t, or (EP) row t0 + t of every rank's gathered states
       const float tot = block_sum(ss, s_red);
       const float r = rsqrtf(tot / static_cast<float>(d_h) + eps);
+      const int ndst = ep.world ? ep.world : 1;
       if (base == 0) {
 #pragma unroll
         for (int c = 0; c < kRowChunks; ++c) {
           const int f0 = row_chunk(base, c);
           if (f0 >= d_h) continue;
-          const size_t o = static_cast<size_t>(t) * d_h + f0;
           float hv[4] = {acc[c][0] * r, acc[c][1] * r, acc[c][2] * r, acc[c][3] * r};
-          if (vec4 && f0 + 4 <= d_h) store_bf16x4(h_next + o, hv);
-          else for (int q = 0; q < 4 && f0 + q < d_h; ++q) h_next[o + q] = __float2bfloat16_rn(hv[q]);
+          for (int p = 0; p < ndst; ++p) {
+            __nv_bfloat16* hd = (ep.world ? ep.h_all[p] + static_cast<size_t>(ep.t0 + t) * d_h
+                                          : h_next + static_cast<size_t>(t) * d_h) + f0;
+            if (vec4 && f0 + 4 <= d_h) store_bf16x4(hd, hv);
+            else for (int q = 0; q < 4 && f0 + q < d_h; ++q) hd[q] = __float2bfloat16_rn(hv[q]);
+          }
         }
         return;
       }
@@ -291,8 +329,10 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
         for (int c = 0; c < kRowChunks; ++c) {
           const int f0 = row_chunk(b2, c);
           for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
-            const size_t o = static_cast<size_t>(t) * d_h + f0 + q;
-            h_next[o] = __float2bfloat16_rn(x_res[o] * r);
+            const float hv = x_res[static_cast<size_t>(t) * d_h + f0 + q] * r;
+            for (int p = 0; p < ndst; ++p)
+              (ep.world ? ep.h_all[p] + static_cast<size_t>(ep.t0 + t) * d_h
+                        : h_next + static_cast<size_t>(t) * d_h)[f0 + q] = __float2bfloat16_rn(hv);
           }
         }
       return;
@@ -303,10 +343,12 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const EpPeers* ep, const int32_t* ids_rr) {
   if (T <= 0) return cudaSuccess;
+  EpPeers none{};
   return launch_pdl(g_pdl, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
-                    d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps);
+                    d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps,
+                    ep ? *ep : none, ids_rr);
 }
 
 }  // namespace sere

@@ -71,6 +71,23 @@ inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+// Expert-parallel group seen through NVLink peer memory (ep_p2p.cu; world == 0: single GPU).
+// Every pointer array is indexed by rank; entry `rank` is this rank's own buffer.
+constexpr int kMaxEpRanks = 8;
+struct EpPeers {
+  int world, rank;
+  int t0, T_all;                      // this rank's first global token; tokens of the whole batch
+  int e_lo[kMaxEpRanks + 1];          // routed-expert blocks: rank r owns [e_lo[r], e_lo[r+1])
+  int nsh[kMaxEpRanks];               // shared experts owned by rank r (s % world == r)
+  int r_max[kMaxEpRanks];             // rank r's permuted-row capacity (its y_perm split stride / d_h_pad)
+  const float* y_perm[kMaxEpRanks];   // rank r's down-GEMM outputs
+  const int32_t* slot_row[kMaxEpRanks];
+  __nv_bfloat16* h_all[kMaxEpRanks];  // rank r's gathered token states [T_all][d_h]
+  int32_t* ids_all[kMaxEpRanks];      // rank r's gathered router ids [T_all][K]
+  float* w_all[kMaxEpRanks];          // rank r's gathered router weights [T_all][K]
+  int32_t* flags[kMaxEpRanks];        // rank r's barrier flags [world]
+};
+
 extern bool g_pdl;  // capi.cu: PDL on the layer chain (sere_set_pdl)  // router.cu: debug phase clocks of the router (nullptr = off)
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
@@ -82,7 +99,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
-                           cudaStream_t stream);
+                           cudaStream_t stream, const EpPeers* ep = nullptr, const int32_t* ids_rr = nullptr);
 cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream);
 size_t moe_ffn_smem(int Et);
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
@@ -90,7 +107,9 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
                               cudaStream_t stream);
 cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
                              int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out, void* ws,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const EpPeers* ep = nullptr);
+cudaError_t launch_ep_barrier(const EpPeers& ep, int32_t* epoch, int32_t* status, long long timeout_ns,
+                              cudaStream_t stream);
 size_t route_workspace_bytes(int T, int d_h, int M);
 bool route_fast_path(int M, int K, int d_h);
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,

@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
                                                                    int M, int K, int kc,
                                                                    int32_t* __restrict__ ids,
                                                                    float* __restrict__ weights,
-                                                                   float* __restrict__ logits_out, long long* dbg) {
+                                                                   float* __restrict__ logits_out, long long* dbg,
+                                                                   const EpPeers ep) {
   extern __shared__ __align__(16) uint8_t rsm[];
   const int LD = kc + kRcPad;  // padded row (bank-conflict-free fragment loads)
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(rsm);  // [16][LD]
@@ -321,8 +322,18 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
       for (int k = 0; k < K; ++k) den += __expf(sel_v[r * K + k] - top);
       if (lane < K) {
         const size_t o = static_cast<size_t>(t0 + my_t0 + r) * K + lane;
-        ids[o] = sel_i[r * K + lane];
-        weights[o] = __expf(sel_v[r * K + lane] - top) / den;
+        const int id = sel_i[r * K + lane];
+        const float wv = __expf(sel_v[r * K + lane] - top) / den;
+        if (ep.world == 0) {
+          ids[o] = id;
+          weights[o] = wv;
+        } else {  // expert parallel: this rank's rows of every rank's gathered table (NVLink stores)
+          const size_t og = static_cast<size_t>(ep.t0) * K + o;
+          for (int p = 0; p < ep.world; ++p) {
+            ep.ids_all[p][og] = id;
+            ep.w_all[p][og] = wv;
+          }
+        }
       }
     }
   }
@@ -338,7 +349,7 @@ bool route_fast_path(int M, int K, int d_h) {
 
 cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,
                              int d_h, int M, int K, int32_t* ids, float* weights, float* logits_out, void* ws,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const EpPeers* ep) {
   (void)ws;
   if (T <= 0) return cudaSuccess;
   const RouteGeom g = route_geom(d_h, M);
@@ -363,8 +374,9 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_pdl ? 2 : 1;
+  EpPeers none{};
   return cudaLaunchKernelEx(&cfg, route_cluster_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
-                            logits_out, g_route_dbg);
+                            logits_out, g_route_dbg, ep ? *ep : none);
 }
 
 cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_router, const float* bias, int T,

@@ -116,3 +116,25 @@ def test_product_never_imports_oracle():
         src = p.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+([\w\.]+)", src, flags=re.M), p
         assert "sere_oracle" not in src, p
+
+
+def test_ep_peers_struct_matches_c_header(tmp_path):
+    """ctypes `EpPeers` mirrors `sere_ep_peers` (size and field offsets, compiled with gcc)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2602_07616_b200 import _lib
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "probe.c"
+    fields = [f for f, _ in _lib.EpPeers._fields_]
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "sere_b200.h"\nint main(void){'
+                   + 'printf("%zu", sizeof(sere_ep_peers));'
+                   + "".join(f'printf(" %zu", offsetof(sere_ep_peers, {f}));' for f in fields) + "return 0;}\n")
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(_lib.EpPeers)
+    assert vals[1:] == [getattr(_lib.EpPeers, f).offset for f in fields]
