@@ -60,6 +60,8 @@ def parse_args():
     ap.add_argument("--threshold", type=float, default=0.5)
     ap.add_argument("--beta", type=float, default=1.0, help="router popularity skew (SURVEY Appendix C)")
     ap.add_argument("--sim", choices=["uniform", "clustered"], default="uniform")
+    ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
+                    help="expert-parallel transport for N>1: peer-memory kernels (ep_p2p) or NCCL collectives (ep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     a = ap.parse_args()
@@ -311,6 +313,12 @@ def run_ours(args, wl):
     t_build = time.perf_counter() - t_build
 
     def make_step(mode):
+        if world > 1 and args.ep == "p2p":
+            from paper_2602_07616_b200.ep_p2p import P2PDecodeStep
+
+            st = P2PDecodeStep(model, T, world, rank, args.retain, args.threshold, mode)
+            st.connect_ipc()
+            return st
         if world > 1:
             return ep.EPDecodeStep(model, T, args.retain, args.threshold, mode)
         return decode.DecodeStep(model, T, args.retain, args.threshold, mode)
@@ -318,16 +326,28 @@ def run_ours(args, wl):
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1)
     x_full = torch.randn((T, wl["d_h"]), generator=gen, device="cuda")
-    sere = make_step("sere")
-    topk = make_step("topk")
-    t_local = sere.T_local if world > 1 else T
-    x_local = x_full[rank * t_local:(rank + 1) * t_local].contiguous()
-    sere.x_in.copy_(x_local)
-    topk.x_in.copy_(x_local)
-    graphed = []
-    for st in (sere, topk):
-        ok = st.capture()
-        graphed.append(True if ok is None else bool(ok))
+    transport = args.ep if world > 1 else "none"
+
+    def make_pair():
+        sere, topk = make_step("sere"), make_step("topk")
+        t_local = sere.T_local if world > 1 else T
+        x_local = x_full[rank * t_local:(rank + 1) * t_local].contiguous()
+        sere.x_in.copy_(x_local)
+        topk.x_in.copy_(x_local)
+        graphed = []
+        for st in (sere, topk):
+            ok = st.capture()
+            graphed.append(True if ok is None else bool(ok))
+        return sere, topk, x_local, graphed
+
+    try:
+        sere, topk, x_local, graphed = make_pair()
+    except Exception as exc:  # peer memory unavailable on this node: same kernels, NCCL transport
+        if transport != "p2p":
+            raise
+        print(f"[bench] peer-memory EP unavailable ({exc}); using NCCL collectives", file=sys.stderr)
+        args.ep = transport = "nccl"
+        sere, topk, x_local, graphed = make_pair()
 
     clocks = ClockSampler(local)
     for _ in range(args.warmup):
@@ -411,15 +431,19 @@ def run_ours(args, wl):
         sere.run()
         torch.cuda.synchronize()
         bank = model.layers[-1].bank
-        ws = _moe_mod.workspace(T, wl["K"], bank.M, bank.n_shared, wl["d_h"], wl["d_m"], bank.device)
+        if hasattr(sere, "workspace"):  # peer-memory EP: the workspace lives in the rank's peer region
+            ws_ptr, ws_bytes = sere.workspace
+        else:
+            ws = _moe_mod.workspace(T, wl["K"], bank.M, bank.n_shared, wl["d_h"], wl["d_m"], bank.device)
+            ws_ptr, ws_bytes = ws.data_ptr(), ws.numel()
         stream = torch.cuda.current_stream()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         lib.call("sere_debug_replay_ffn", bank.data.data_ptr(), bank.M, bank.n_shared, wl["d_h"], wl["d_m"], 0, T,
-                 wl["K"], ws.data_ptr(), ws.numel(), 2, stream.cuda_stream)  # warm
+                 wl["K"], ws_ptr, ws_bytes, 2, stream.cuda_stream)  # warm
         clocks.start()
         ev0.record(stream)
         lib.call("sere_debug_replay_ffn", bank.data.data_ptr(), bank.M, bank.n_shared, wl["d_h"], wl["d_m"], 0, T,
-                 wl["K"], ws.data_ptr(), ws.numel(), reps, stream.cuda_stream)
+                 wl["K"], ws_ptr, ws_bytes, reps, stream.cuda_stream)
         ev1.record(stream)
         torch.cuda.synchronize()
         clocks.pause()
@@ -480,7 +504,7 @@ def run_ours(args, wl):
                    "d_h": wl["d_h"], "d_m": wl["d_m"], "shared_experts": wl["n_shared"],
                    "retain_S": args.retain, "threshold_rho": args.threshold, "router_skew_beta": args.beta,
                    "sim": args.sim, "block": "prenorm_residual (RMSNorm -> router -> SERE -> grouped FFN -> +x)",
-                   "parallelism": f"ep{world}", "l2": "no flush: 58 GB of expert weights per step >> 126 MB L2",
+                   "parallelism": f"ep{world}", "ep_transport": transport, "l2": "no flush: 58 GB of expert weights per step >> 126 MB L2",
                    "cuda_graph": all(graphed)},
         "topk": {"value": round(tok_s_topk, 1), "unit": "tokens/s", "ms_per_step": round(ms_topk, 4),
                  "active_experts_per_layer": round(float(act_topk.mean()), 2)},

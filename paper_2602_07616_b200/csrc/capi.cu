@@ -467,11 +467,14 @@ int sere_combine_ep(const sere_ep_peers* peers, const int32_t* ids_rr, const voi
   if (!ids_rr || !workspace || !x_res) return SERE_ERR_DIMENSION;
   const WsLayout L = ws_layout(ep.T_all, K, M_local, n_shared_local, d_h, d_m);
   uint8_t* ws = ws_base(workspace);
-  return check_cuda(launch_combine(reinterpret_cast<const float*>(ws + L.y_perm), L.d, L.r_max,
-                                   reinterpret_cast<const int32_t*>(ws + L.plan),
-                                   reinterpret_cast<const int32_t*>(ws + L.slot_row), ep.w_all[ep.rank], T_local, K,
-                                   n_shared_total, y_local, nullptr, x_res, nullptr, eps,
-                                   static_cast<cudaStream_t>(stream), &ep, ids_rr));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  stage_mark(4, st);
+  const cudaError_t e = launch_combine(reinterpret_cast<const float*>(ws + L.y_perm), L.d, L.r_max,
+                                       reinterpret_cast<const int32_t*>(ws + L.plan),
+                                       reinterpret_cast<const int32_t*>(ws + L.slot_row), ep.w_all[ep.rank], T_local,
+                                       K, n_shared_total, y_local, nullptr, x_res, nullptr, eps, st, &ep, ids_rr);
+  stage_mark(5, st);
+  return check_cuda(e);
 }
 
 int sere_alloc_peer(size_t bytes, void** out) {

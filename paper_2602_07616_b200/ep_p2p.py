@@ -33,6 +33,7 @@ import numpy as np
 from . import _lib
 from . import moe as _moe
 from . import rerouting as _rr
+from .decode import StageEvents
 from .ep import expert_range, shared_owned, token_slice
 
 
@@ -115,7 +116,7 @@ class PeerRegion:
             self.base = 0
 
 
-class P2PDecodeStep:
+class P2PDecodeStep(StageEvents):
     """One rank's expert-parallel decode step over peer memory (prenorm-residual block,
     the same layer chain as `decode.DecodeStep`, whose output it reproduces bit for bit)."""
 
@@ -250,6 +251,7 @@ class P2PDecodeStep:
             self._barrier()
             if self._ffn_pre is not None:
                 self._ffn_pre(l)
+            self._events_on(l)  # stages 0-3 inside sere_moe_ffn_ep, 4-5 around the combine
             out = self.outs[l]
             rr = out.reroute
             dsim = layer.sim
@@ -268,6 +270,7 @@ class P2PDecodeStep:
             _lib.call("sere_combine_ep", ctypes.byref(self.peers), rr.new_indices.data_ptr(), reg.ws_ptr,
                       self.hi - self.lo, bank.n_shared, self.n_shared_total, d_h, m.d_m, K, self.x.data_ptr(), None,
                       ctypes.c_float(self.eps), _moe._stream_ptr())
+            self._events_off()
 
     @property
     def launches_per_step(self) -> int:
@@ -280,6 +283,29 @@ class P2PDecodeStep:
             self.graph.replay()
         else:
             self._launch()
+
+    def capture(self) -> bool:
+        """Warm up, then capture the whole step (barriers and peer loads/stores are plain
+        kernels, so the graph replays on every rank in lockstep)."""
+        torch = _torch()
+        self._launch()
+        torch.cuda.synchronize()
+        self.check()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch()
+        self.graph = g
+        return True
+
+    def run_host(self, x_host, out_host) -> None:
+        self.x_in.copy_(x_host, non_blocking=True)
+        self.run()
+        out_host.copy_(self.x, non_blocking=True)
+
+    @property
+    def workspace(self) -> tuple[int, int]:
+        """(device pointer, bytes) of this rank's layer workspace (kernel-only FFN replay)."""
+        return self.region.ws_ptr, self.region.ws_bytes
 
     def check(self) -> None:
         from .errors import raise_for_status
