@@ -177,6 +177,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.e_lo = e_lo;
   ap.m_local = m_local;
   ap.r_max = L.r_max;
+  ap.ffn_ctas = sms;
   ap.dbg = g_align_dbg;
   stage_mark(0, stream);
   cudaError_t e = launch_reroute_align(ap, stream);

@@ -97,14 +97,14 @@ struct __align__(16) FfnSmemTail {
   int32_t n_groups, units_gu, units_dn;
 };
 
-// per-schedule-position copies of the plan (6 arrays of Et + 1)
+// per-schedule-position copies of the plan (7 arrays of Et + 1)
 __host__ __device__ inline size_t ffn_smem_bytes(int Et) {
   return 1024 /*align slack*/ + static_cast<size_t>(kPages) * kPageBytes + sizeof(FfnSmemTail) +
-         static_cast<size_t>(6) * (Et + 1) * sizeof(int32_t);
+         static_cast<size_t>(7) * (Et + 1) * sizeof(int32_t);
 }
 
 struct SchedView {
-  const int32_t *uoff_gu, *uoff_dn, *gid, *gexp, *grow0, *grows;
+  const int32_t *uoff_gu, *uoff_dn, *gid, *gexp, *grow0, *grows, *mw_gu;
 };
 
 __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, const SchedView& v,
@@ -123,7 +123,7 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
   const int n16 = round_up(rows, kRowAlign);
   const int ncb = col_blocks(n16);
   const int tiles = U.dn ? p.tiles_dn : p.tiles_gu;
-  const int mw = unit_mw(n16, U.dn ? dn_cap(n16) : kMwGuMax, tiles, U.dn ? 1 : 2);
+  const int mw = unit_mw(n16, U.dn ? dn_cap(n16) : v.mw_gu[lo], tiles, U.dn ? 1 : 2);
   const int nc = local % ncb;
   const int tmp = local / ncb;
   const int ksplit = U.dn ? p.ksplit_dn : 1;
@@ -140,7 +140,7 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
   const int kchunk = (ktiles + ksplit - 1) / ksplit;
   U.kt_begin = U.ks * kchunk;
   U.kt_end = min(ktiles, U.kt_begin + kchunk);
-  U.need = group_units_gu(n16, p.tiles_gu);  // gate/up units of this group (the down units' dependency)
+  U.need = group_units_gu(n16, p.tiles_gu, v.mw_gu[lo]);  // gate/up units of this group (the down units' dependency)
   return U;
 }
 
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kPages * kPageBytes);
   int32_t* s_arr = reinterpret_cast<int32_t*>(tail + 1);
   const int E1 = p.Et + 1;
-  SchedView sv{s_arr, s_arr + E1, s_arr + 2 * E1, s_arr + 3 * E1, s_arr + 4 * E1, s_arr + 5 * E1};
+  SchedView sv{s_arr, s_arr + E1, s_arr + 2 * E1, s_arr + 3 * E1, s_arr + 4 * E1, s_arr + 5 * E1, s_arr + 6 * E1};
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PlanOffsets po = plan_offsets(p.Et);
@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       const_cast<int32_t*>(sv.gexp)[i] = plan[po.group_expert + g];
       const_cast<int32_t*>(sv.grow0)[i] = plan[po.group_row0 + g];
       const_cast<int32_t*>(sv.grows)[i] = plan[po.group_rows + g];
+      const_cast<int32_t*>(sv.mw_gu)[i] = plan[po.mw_gu + i];
     }
   }
   tc_fence_before();

@@ -32,6 +32,7 @@ struct AlignParams {
   int tiles_gu, tiles_dn, ksplit_dn;  // FFN geometry (work units: plan.cuh group_units_*)
   int e_lo, m_local; // expert-parallel ownership: bank holds global experts [e_lo, e_lo+m_local)
   int r_max;         // rows of the permuted batch buffer (row_token is staged in smem when it fits)
+  int ffn_ctas;      // grid of the fused FFN (its first wave of gate/up units)
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
 };
 

@@ -20,6 +20,8 @@
 //   unit_off_gu/dn[Et+1]  prefix of work units over the schedule order
 //   dep[Et]               gate/up units finished per group (the down units of a group
 //                         wait for all of them); zeroed by align
+//   mw_gu[Et]             feature blocks per gate/up unit by schedule position (kMwGuMax;
+//                         SERE_TAIL_MW1: 1 for groups that miss the FFN's first wave)
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -39,7 +41,7 @@ enum PlanIdx : int {
 };
 
 struct PlanOffsets {
-  int counts, group_expert, group_row0, group_rows, sched, unit_off_gu, unit_off_dn, dep, total;
+  int counts, group_expert, group_row0, group_rows, sched, unit_off_gu, unit_off_dn, dep, mw_gu, total;
 };
 
 __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
@@ -52,7 +54,8 @@ __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
   o.unit_off_gu = o.sched + Et;
   o.unit_off_dn = o.unit_off_gu + Et + 1;
   o.dep = o.unit_off_dn + Et + 1;
-  o.total = o.dep + Et;
+  o.mw_gu = o.dep + Et;
+  o.total = o.mw_gu + Et;
   return o;
 }
 
@@ -89,8 +92,8 @@ __host__ __device__ inline int unit_mw(int n16, int cap, int tiles, int accs = 1
   return mw < 1 ? 1 : mw;
 }
 __host__ __device__ inline int col_blocks(int n16) { return (n16 + kColBlock - 1) / kColBlock; }
-__host__ __device__ inline int group_units_gu(int n16, int tiles_gu) {
-  const int mw = unit_mw(n16, kMwGuMax, tiles_gu, 2);
+__host__ __device__ inline int group_units_gu(int n16, int tiles_gu, int cap = kMwGuMax) {
+  const int mw = unit_mw(n16, cap, tiles_gu, 2);
   return col_blocks(n16) * ((tiles_gu + mw - 1) / mw);
 }
 #ifndef SERE_DN_SMALL_N

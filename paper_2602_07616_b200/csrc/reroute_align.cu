@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   __syncthreads();
   SERE_PHASE(11);
   if (warp == nwarps - 1) {  // unit prefixes over the schedule order (a warp idle in pass 2 for T < 992)
-    int gu_base = 0, dn_base = 0;
+    int gu_base = 0, dn_base = 0, gu2_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
       int ugu = 0, udn = 0;
@@ -403,6 +403,16 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         ugu = s_ugu[i];
         udn = s_udn[i];
       }
+#ifndef SERE_TAIL_MW1
+#define SERE_TAIL_MW1 0
+#endif
+      const int gu2_in = warp_incl_scan(ugu);
+      if (i < G) {
+        const int cap = (!SERE_TAIL_MW1 || gu2_base + gu2_in <= p.ffn_ctas) ? kMwGuMax : 1;
+        if (cap != kMwGuMax) ugu = group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, cap);
+        plan[po.mw_gu + i] = cap;
+      }
+      gu2_base += __shfl_sync(0xffffffffu, gu2_in, 31);
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {
         plan[po.unit_off_gu + i] = gu_base + gu_in - ugu;
