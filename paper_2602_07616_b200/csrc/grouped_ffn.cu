@@ -271,6 +271,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (done) {
           if (tr) { tr[1] = w_empty + w_empty_dn; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; tr[1018] = w_empty_dn; }
+#if SERE_PDL_COMBINE
+          // no work left for this CTA: once every CTA got here, the combine grid may launch
+          // onto the SMs the FFN has already left and stage its slots (it waits for the FFN
+          // grid to complete before touching y_perm)
+          pdl_trigger();
+#endif
           break;
         }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);

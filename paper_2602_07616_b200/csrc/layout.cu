@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
       s_w[k] = k < K ? w[t * K + k] : 1.f;
     }
   } else {
+    pdl_wait();  // peers' slot rows are ordered by the barrier kernel before us: wait for it
     const int tg = ep.t0 + t, TK = ep.T_all * K;
     for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
       int o, idx;
@@ -346,7 +347,7 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            cudaStream_t stream, const EpPeers* ep, const int32_t* ids_rr) {
   if (T <= 0) return cudaSuccess;
   EpPeers none{};
-  return launch_pdl(g_pdl, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
+  return launch_pdl(g_pdl || SERE_PDL_COMBINE, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
                     d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps,
                     ep ? *ep : none, ids_rr);
 }

@@ -89,6 +89,13 @@ struct EpPeers {
   int32_t* flags[kMaxEpRanks];        // rank r's barrier flags [world]
 };
 
+// 1: the combine grid is launched with programmatic dependent launch and the FFN triggers
+// it when each CTA runs out of tickets, so combine CTAs start on the SMs the FFN's tail has
+// left and stage their slots. Measured within noise on the 48-layer bench (-1.2% on a
+// 24-layer kernel trace), so off by default; an early trigger slowed the FFN.
+#ifndef SERE_PDL_COMBINE
+#define SERE_PDL_COMBINE 0
+#endif
 extern bool g_pdl;  // capi.cu: PDL on the layer chain (sere_set_pdl)  // router.cu: debug phase clocks of the router (nullptr = off)
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
