@@ -216,25 +216,29 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     // ---- rewrite the secondary cells (weights are never touched) + outputs
     bool bad = false;
     const bool vec_out = vec && (reinterpret_cast<uintptr_t>(p.ids_out) & 15) == 0;
-    for (int t = tid; t < T; t += nthr) {
-      for (int k = S; k < K; ++k) {
-        const int e = s_ids[k * T + t];
-        if (s_cls[e] & SERE_CLASS_REROUTED) {
-          const int v = s_map[e];
-          s_ids[k * T + t] = v;
-          bad |= (v < 0 || v >= M);  // reference NaN quirk: a secondary mapped to -1
+    // one work item per (token, 4-slot quad): T * ceil(K/4) items keep all threads busy
+    const int nq = (K + 3) >> 2;
+    for (int it = tid; it < T * nq; it += nthr) {
+      const int t = it / nq, k0 = (it - t * nq) * 4;
+      int v4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        v4[j] = 0;
+        if (k < K) {
+          int e = s_ids[k * T + t];
+          if (k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
+            e = s_map[e];
+            s_ids[k * T + t] = e;
+            bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
+          }
+          v4[j] = e;
         }
       }
       if (p.ids_out) {
-        int32_t* dst = p.ids_out + static_cast<size_t>(t) * K;
-        for (int k0 = 0; k0 < K; k0 += 4) {
-          if (vec_out) {
-            *reinterpret_cast<int4*>(dst + k0) = make_int4(s_ids[k0 * T + t], s_ids[(k0 + 1) * T + t],
-                                                           s_ids[(k0 + 2) * T + t], s_ids[(k0 + 3) * T + t]);
-          } else {
-            for (int k = k0; k < K && k < k0 + 4; ++k) dst[k] = s_ids[k * T + t];
-          }
-        }
+        int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
+        if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
       }
     }
     if (bad) s_err_route = 1;
@@ -437,9 +441,11 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   int32_t* s_rt = reinterpret_cast<int32_t*>(smem + align_smem_bytes(T, K, M, Et));
   int32_t* rt = stage ? s_rt : p.row_token;
   const bool vec_sr = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(p.slot_row) & 15) == 0;
-  for (int t = tid; t < T; t += nthr) {
+  const int nq = (K + 3) >> 2;  // one work item per (token, 4-slot quad)
+  for (int it = tid; it < T * nq; it += nthr) {
+    const int t = it / nq, k0 = (it - t * nq) * 4;
     const int tb = t / kTokBlk;
-    for (int k0 = 0; k0 < K; k0 += 4) {
+    {
       int rows4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -457,11 +463,12 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       if (vec_sr) *reinterpret_cast<int4*>(dst) = make_int4(rows4[0], rows4[1], rows4[2], rows4[3]);
       else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = rows4[j];
     }
-    for (int s = 0; s < p.n_shared; ++s) {  // shared experts: every token, in token order
-      const int row = s_row0[m_loc + s] + t;
-      p.slot_row[TK + t * p.n_shared + s] = row;
-      rt[row] = t;
-    }
+  }
+  for (int it = tid; it < T * p.n_shared; it += nthr) {  // shared experts: every token, in token order
+    const int t = it / p.n_shared, s = it - t * p.n_shared;
+    const int row = s_row0[m_loc + s] + t;
+    p.slot_row[TK + t * p.n_shared + s] = row;
+    rt[row] = t;
   }
   for (int e = warp; e < Et; e += nwarps) {  // padding rows of each group
     const int cnt = s_cnt[e];
