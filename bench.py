@@ -340,14 +340,22 @@ def run_ours(args, wl):
             graphed.append(True if ok is None else bool(ok))
         return sere, topk, x_local, graphed
 
+    ok, err = 1, None
     try:
         sere, topk, x_local, graphed = make_pair()
     except Exception as exc:  # peer memory unavailable on this node: same kernels, NCCL transport
         if transport != "p2p":
             raise
-        print(f"[bench] peer-memory EP unavailable ({exc}); using NCCL collectives", file=sys.stderr)
-        args.ep = transport = "nccl"
-        sere, topk, x_local, graphed = make_pair()
+        ok, err = 0, exc
+    if transport == "p2p":  # every rank takes the same transport
+        import torch.distributed as dist
+
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            print(f"[bench] peer-memory EP unavailable ({err}); using NCCL collectives", file=sys.stderr)
+            args.ep = transport = "nccl"
+            sere, topk, x_local, graphed = make_pair()
 
     clocks = ClockSampler(local)
     for _ in range(args.warmup):
