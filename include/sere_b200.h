@@ -214,6 +214,10 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf);
 /* Debug experiments on the fused FFN (outputs become INVALID): bit0 = skip the weight
  * copies, bit1 = skip the MMAs. 0 = normal operation. */
 int sere_debug_set_ffn_mode(int mode);
+/* Experiment: gate/up activation rows gathered from the layer input inside the fused FFN
+ * (a gather warp, 16-B cp.async per row chunk) instead of the permute kernel. Results are
+ * bit-identical; measured slower, so 0 (off) is the default. */
+int sere_debug_set_ffn_gather(int enable);
 /* Debug: router phase clocks (clock64) per CTA, dev_buf[cta * 8 + phase]. NULL disables. */
 int sere_debug_set_route_clocks(int64_t* dev_buf);
 /* Kernel-only timing: relaunch the fused expert FFN `reps` times on the plan and operands

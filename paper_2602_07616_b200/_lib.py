@@ -107,6 +107,7 @@ SIGNATURES = {
     "sere_debug_set_align_clocks": (_c_int, [_p]),
     "sere_debug_set_ffn_trace": (_c_int, [_p]),
     "sere_debug_set_ffn_mode": (_c_int, [_c_int]),
+    "sere_debug_set_ffn_gather": (_c_int, [_c_int]),
     "sere_debug_set_route_clocks": (_c_int, [_p]),
     "sere_set_pdl": (_c_int, [_c_int]),
     "sere_debug_replay_ffn": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_size,

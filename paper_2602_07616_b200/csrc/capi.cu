@@ -37,6 +37,15 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 long long* g_align_dbg = nullptr;  // sere_debug_set_align_clocks
 unsigned long long* g_ffn_trace = nullptr;  // sere_debug_set_ffn_trace
 int g_ffn_dbg_mode = 0;                     // sere_debug_set_ffn_mode
+#ifndef SERE_GATHER_X
+#define SERE_GATHER_X 0
+#endif
+// gather mode: the FFN's gather warp reads gate/up activation rows from x via row_token,
+// replacing the permute kernel and x_pack (FfnParams::gather). Bit-identical results, but
+// measured 45% slower FFN (99 -> 143 us on a 56-active C4 layer): one warp's 16-B cp.async
+// stream cannot keep up with the weight stream, so it is off (sere_debug_set_ffn_gather)
+bool g_ffn_gather = SERE_GATHER_X != 0;
+const void* g_last_x = nullptr;  // the last layer input (sere_debug_replay_ffn in gather mode)
 
 constexpr int kStageEvents = 6;
 thread_local cudaEvent_t t_stage_events[kStageEvents];
@@ -129,6 +138,9 @@ FfnParams ffn_params(const void* bank, const WsLayout& L, uint8_t* ws, int activ
   fp.act = activation;
   fp.trace = g_ffn_trace;
   fp.dbg_mode = g_ffn_dbg_mode;
+  fp.row_token = reinterpret_cast<const int32_t*>(ws + L.row_token);
+  fp.x_row_bytes = L.d.d_h * 2;
+  fp.d_h = L.d.d_h;
   return fp;
 }
 
@@ -184,10 +196,18 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   stage_mark(1, stream);
-  e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
-  if (e != cudaSuccess) return SERE_ERR_CUDA;
+  const bool gather = g_ffn_gather && d_h % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  if (!gather) {
+    e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
+    if (e != cudaSuccess) return SERE_ERR_CUDA;
+  }
 
   FfnParams fp = ffn_params(bank, L, ws, activation);
+  if (gather) {
+    fp.gather = 1;
+    fp.x = reinterpret_cast<const uint8_t*>(x);
+    g_last_x = x;
+  }
   stage_mark(2, stream);
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -541,6 +561,12 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
   return SERE_OK;
 }
 
+int sere_debug_set_ffn_gather(int enable) {
+  g_ffn_gather = enable != 0;
+  if (!g_ffn_gather) g_last_x = nullptr;
+  return SERE_OK;
+}
+
 int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, int T, int K,
                           void* workspace, size_t workspace_bytes, int reps, void* stream) {
   int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
@@ -548,7 +574,11 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
   if (!bank || !workspace || reps < 0) return SERE_ERR_DIMENSION;
   const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
   if (workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
-  const FfnParams fp = ffn_params(bank, L, ws_base(workspace), activation);
+  FfnParams fp = ffn_params(bank, L, ws_base(workspace), activation);
+  if (g_ffn_gather && g_last_x != nullptr && d_h % 8 == 0) {
+    fp.gather = 1;
+    fp.x = reinterpret_cast<const uint8_t*>(g_last_x);
+  }
   for (int i = 0; i < reps; ++i) {
     const cudaError_t e = launch_moe_ffn(fp, num_sms(), static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return SERE_ERR_CUDA;

@@ -50,6 +50,12 @@ struct FfnParams {
   int dbg_mode;               // debug experiments (results invalid): bit0 skip weight copies, bit1 skip MMAs,
                               // bit2 skip the expert-output stores
   unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
+  // gather mode (gather != 0): gate/up activation tiles are gathered from the layer input
+  // x [T][d_h] bf16 through row_token by the FFN's gather warp (no permute kernel, no x_pack)
+  int gather;
+  const uint8_t* x;
+  const int32_t* row_token;
+  int x_row_bytes, d_h;
 };
 constexpr int kFfnTraceStride = 2048;
 constexpr int kFfnTraceUnits = 200;
