@@ -26,14 +26,18 @@ def _run(steps, streams):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,n_shared,mode", [(2, 0, "sere"), (4, 2, "sere"), (2, 1, "topk")])
-def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shared, mode):
+@pytest.mark.parametrize("world,n_shared,mode,shape", [(2, 0, "sere", "small"), (4, 2, "sere", "small"),
+                                                       (2, 1, "topk", "small"), (2, 0, "sere", "c4")])
+def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shared, mode, shape):
     import torch
 
     from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
     from paper_2602_07616_b200.ep_p2p import P2PDecodeStep
 
-    L, M, K, d_h, d_m, T = 3, 32, 4, 512, 256, 64
+    if shape == "c4":  # the Qwen3-30B-A3B layer shape (2 layers, half the decode batch)
+        L, M, K, d_h, d_m, T = 2, 128, 8, 2048, 768, 256
+    else:
+        L, M, K, d_h, d_m, T = 3, 32, 4, 512, 256, 64
     ref = DecodeStep(DecodeModel(L, M, K, d_h, d_m, n_shared=n_shared, seed=4, beta=1.0), T, 1, 0.5, mode)
     steps = [P2PDecodeStep(m, T, world, r, 1, 0.5, mode) for r, m in enumerate(_shards(L, M, K, d_h, d_m,
                                                                                         n_shared, world))]
@@ -55,6 +59,7 @@ def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shar
             got = torch.cat([st.x for st in steps])
             assert torch.equal(got, ref.x), (it, (got - ref.x).abs().max().item())
         assert all(int(st.epoch.item()) == 2 * 2 * L for st in steps)
+        del ref
     finally:
         for st in steps:
             st.close()
