@@ -321,3 +321,66 @@ def random_assignment(rng: np.random.Generator, t: int, k: int, m: int):
     """tests/test_rerouting.py:32-34: top-k of a random 4-wide router."""
     w_router = rng.standard_normal((4, m))
     return route_topk(w_router, k, rng.standard_normal((t, 4)))
+
+
+# ---------------------------------------------------------------------------
+# similarity calibration (SURVEY §8(f4); offline, activation-based)
+# ---------------------------------------------------------------------------
+
+def gaussian_batches(seed: int, n_batches: int, tokens_per_batch: int, d_h: int) -> list:
+    """similarity.py:298-306: deterministic standard-normal calibration batches."""
+    rng = np.random.default_rng(seed)
+    return [rng.standard_normal((tokens_per_batch, d_h)) for _ in range(n_batches)]
+
+
+def _pair_raw(a: np.ndarray, b: np.ndarray, metric: str) -> float:
+    """similarity.py:127-152, 262-270 (frobenius distance / mean row cosine)."""
+    if metric == "frobenius":
+        d = a - b
+        return float(np.sqrt((d * d).sum()))
+    if metric == "cosine":
+        num = (a * b).sum(axis=1)
+        na = np.sqrt((a * a).sum(axis=1))
+        nb = np.sqrt((b * b).sum(axis=1))
+        denom = na * nb
+        safe = np.where(denom > 0.0, denom, 1.0)
+        per_row = np.where(denom > 0.0, num / safe, 0.0)
+        return float(per_row.sum() / a.shape[0])
+    raise ValueError(metric)
+
+
+def estimate_similarity_raw(layers, batches, metric: str, activation: str = "silu") -> list:
+    """similarity.py:325-371: per batch and layer, every routed expert runs densely on the
+    layer input, each unordered pair (diagonal once) is scored and accumulated, and the batch
+    advances through the routed forward (route_topk + layer_forward); averaged over batches."""
+    raw = [np.zeros((len(l.experts), len(l.experts))) for l in layers]
+    for batch in batches:
+        x = np.asarray(batch, dtype=np.float64)
+        for li, layer in enumerate(layers):
+            slabs = [expert_forward(e, x, activation) for e in layer.experts]
+            m = len(slabs)
+            for p in range(m):
+                for q in range(p, m):
+                    s = _pair_raw(slabs[p], slabs[q], metric)
+                    if p == q:
+                        raw[li][p, p] += s
+                    else:
+                        raw[li][p, q] += s
+                        raw[li][q, p] += s
+            ids, w = route_topk(layer.w_router, layer.top_k, x)
+            x = layer_forward(layer, x, ids, w, activation)
+    return [r / len(batches) for r in raw]
+
+
+def normalize_to_unit(raw: np.ndarray, metric: str) -> np.ndarray:
+    """similarity.py:273-295 (+ frobenius_normalize 155-177): distances -> 1 - d/max(offdiag),
+    cosines -> (c+1)/2 clipped; diagonal exactly 1."""
+    raw = np.asarray(raw, dtype=np.float64)
+    if metric == "frobenius":
+        off = raw[~np.eye(raw.shape[0], dtype=bool)]
+        mx = float(off.max()) if off.size else 0.0
+        values = np.ones_like(raw) if mx == 0.0 else 1.0 - raw / mx
+    else:
+        values = np.clip((raw + 1.0) / 2.0, 0.0, 1.0)
+    np.fill_diagonal(values, 1.0)
+    return values

@@ -18,6 +18,8 @@ so the results are committed here and the tests read only these files:
                       gen_model configs (weights re-derived from the seed by
                       `oracle.sere_oracle.gen_layers`, same draw order).
   topk_cases.npz      topk_softmax outputs incl. ties.
+  calib_cases.npz     estimate_similarity_raw / estimate_similarity (frobenius, cosine)
+                      of a small gen_model on gaussian_batches.
 """
 
 from __future__ import annotations
@@ -166,6 +168,21 @@ def reroute_cases():
     print(f"reroute_cases: {len(meta)} instances")
 
 
+def calib_cases():
+    out = {}
+    seed, L, M, K, d_h, d_m = 21, 2, 8, 2, 64, 96
+    model = moe.gen_model(seed=seed, n_layers=L, n_experts=M, top_k=K, d_h=d_h, d_m=d_m)
+    batches = similarity.gaussian_batches(5, 2, 16, d_h)
+    out["config"] = np.array([seed, L, M, K, d_h, d_m, 5, 2, 16], dtype=np.int64)
+    for metric in ("frobenius", "cosine"):
+        raw = similarity.estimate_similarity_raw(model, batches, metric)
+        sims = similarity.estimate_similarity(model, batches, metric)
+        out[f"{metric}_raw"] = np.stack(raw)
+        out[f"{metric}_sim"] = np.stack([s.values for s in sims])
+    np.savez_compressed(HERE / "calib_cases.npz", **out)
+    print("calib_cases: frobenius, cosine")
+
+
 def layer_cases():
     out = {}
     rows = []
@@ -222,4 +239,5 @@ def topk_cases():
 if __name__ == "__main__":
     reroute_cases()
     layer_cases()
+    calib_cases()
     topk_cases()
