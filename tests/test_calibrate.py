@@ -1,0 +1,70 @@
+"""Similarity calibration: the oracle restatement is pinned to the real
+reference's estimate_similarity (tests/golden/calib_cases.npz); the GPU calibration
+(calibrate.py) matches the oracle run on the same bf16-rounded weights."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import sere_oracle as O
+
+GOLDEN = Path(__file__).resolve().parent / "golden" / "calib_cases.npz"
+
+
+def _case():
+    z = np.load(GOLDEN)
+    seed, L, M, K, d_h, d_m, bseed, nb, tpb = (int(v) for v in z["config"])
+    layers = O.gen_layers(seed, L, M, K, d_h, d_m)
+    batches = O.gaussian_batches(bseed, nb, tpb, d_h)
+    return z, layers, batches
+
+
+@pytest.mark.parametrize("metric", ["frobenius", "cosine"])
+def test_oracle_calibration_matches_reference_golden(metric):
+    z, layers, batches = _case()
+    raw = O.estimate_similarity_raw(layers, batches, metric)
+    np.testing.assert_allclose(np.stack(raw), z[f"{metric}_raw"], rtol=0, atol=1e-12)
+    sims = np.stack([O.normalize_to_unit(r, metric) for r in raw])
+    np.testing.assert_allclose(sims, z[f"{metric}_sim"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("metric", ["frobenius", "cosine"])
+def test_normalize_to_unit_matches_reference(metric):
+    from paper_2602_07616_b200.calibrate import normalize_to_unit
+
+    z = np.load(GOLDEN)
+    for raw, want in zip(z[f"{metric}_raw"], z[f"{metric}_sim"]):
+        np.testing.assert_array_equal(normalize_to_unit(raw, metric), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("metric", ["frobenius", "cosine"])
+def test_gpu_calibration_vs_oracle(cuda_device, metric):
+    import torch
+
+    from paper_2602_07616_b200 import calibrate, io
+    from paper_2602_07616_b200.moe import ExpertBank
+
+    z, layers, batches = _case()
+    rnd = lambda a: torch.as_tensor(a, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+    layers = [O.OracleLayer([O.OracleExpert(rnd(e.w_gate), rnd(e.w_up), rnd(e.w_down)) for e in l.experts],
+                            rnd(l.w_router), l.top_k, []) for l in layers]
+    batches = [rnd(b) for b in batches]
+    gpu_layers = []
+    for l in layers:
+        bank = ExpertBank.from_reference_layer(l, device="cuda")
+        wr = torch.as_tensor(l.w_router, dtype=torch.float32, device="cuda").to(torch.bfloat16)
+        gpu_layers.append(io.GpuLayer(bank, io.GpuRouter(wr, l.top_k)))
+    model = io.GpuModel(gpu_layers, layers[0].w_router.shape[0], "silu")
+    want = [O.normalize_to_unit(r, metric) for r in O.estimate_similarity_raw(layers, batches, metric)]
+    got = calibrate.estimate_similarity(model, batches, metric)
+    for l, (g, w) in enumerate(zip(got, want)):
+        err = float(np.abs(g - w).max())
+        assert err <= (5e-3 if l == 0 else 2e-2), (metric, l, err)
+    # the partner each expert would be re-routed to is (near-)optimal under the oracle's matrix
+    off = ~np.eye(want[0].shape[0], dtype=bool)
+    g0 = np.where(off, got[0], -1.0)
+    w0 = np.where(off, want[0], -1.0)
+    best = g0.argmax(axis=1)
+    assert np.all(w0[np.arange(len(best)), best] >= w0.max(axis=1) - 1e-2)
