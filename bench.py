@@ -258,6 +258,44 @@ def cpu_layer_sample(wl, layer_np, h, sim, S, rho, bias, seconds):
     return float(np.median(times)), len(times)
 
 
+def time_reroute_only(torch, model, retain, threshold, Ts=(64, 512), reps=50):
+    """sere_reroute alone (re-routing without count/align), graph-replayed `reps` times, CUDA
+    events on the capture stream: the paper's kernel-level figure (6 us on H20, T <= 64)."""
+    from paper_2602_07616_b200 import moe as _m
+    from paper_2602_07616_b200 import rerouting as _r
+
+    layer = model.layers[0]
+    out = {}
+    for T in Ts:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(3)
+        x = torch.randn((T, model.d_h), generator=g, device="cuda").to(torch.bfloat16)
+        ids, _ = _m.route_topk_device(layer.w_router_t, x, model.K, bias=layer.bias)
+        res = _r.reroute(ids, layer.sim, retain, threshold)
+        res.check()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            _r.reroute(ids, layer.sim, retain, threshold, stream=s, out=res)
+            s.synchronize()
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(reps):
+                    _r.reroute(ids, layer.sim, retain, threshold, stream=s, out=res)
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out[f"T={T}"] = round(e0.elapsed_time(e1) / reps * 1e3, 2)
+        res.check()
+    out["note"] = ("sere_reroute (primary set, per-secondary fp64 argmax, threshold, rewrite; no count/align), "
+                   f"{reps} launches per CUDA graph, CUDA events; paper: 6 us on H20 at T <= 64")
+    return out
+
+
 def oracle_layer_from_bank(torch, model, l):
     """Layer l of the device model as an fp64 oracle layer (same bf16 values)."""
     import numpy as np
@@ -428,6 +466,12 @@ def run_ours(args, wl):
                 "timing": f"CUDA events per stage, {stage_mode}, last of 3 steps"}
         reroute_us = round(float(st[:, 0].mean() * 1e3), 2)
         del prof
+    reroute_only = None
+    if world == 1:
+        try:
+            reroute_only = time_reroute_only(torch, model, args.retain, args.threshold)
+        except Exception as exc:  # report, never fail the bench line on this extra
+            reroute_only = {"error": str(exc)[:200]}
     # ---- kernel-only FFN timing: relaunch the fused FFN back to back on the plan the last
     # layer of a normal SERE step left in the workspace (it re-arms its own counters), CUDA
     # events on the launch stream around `reps` launches
@@ -520,6 +564,8 @@ def run_ours(args, wl):
                  "weight_bytes_skipped_frac": round(1.0 - float(act_sere.sum() / max(act_topk.sum(), 1)), 4),
                  "speedup_vs_topk": round(ms_topk / ms_sere, 4)},
         "reroute_kernel_us": reroute_us,
+        "reroute_kernel_note": "re-route + count/align kernel per layer (stage events in the step graph)",
+        "reroute_only_us": reroute_only,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(T / (ms_e2e * 1e-3), 1), "unit": "tokens/s",
