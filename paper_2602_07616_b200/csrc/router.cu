@@ -161,6 +161,98 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 long long* g_route_dbg = nullptr;  // sere_debug_set_route_clocks: per-CTA phase clock64 [cta][8]
 #define RC_PROBE(i) do { if (dbg && threadIdx.x == 0) dbg[(blockIdx.x * gridDim.y + blockIdx.y) * 8 + (i)] = clock64(); } while (0)
 
+// Split-K partials -> logits -> top-K + softmax, shared by both router kernels: the tile's
+// tokens are spread over the cluster (CTA q owns tokens [q*tpc, (q+1)*tpc)); every CTA
+// bulk-copies each owner its rows of this split's partial over distributed shared memory
+// (S-1 copies per CTA, into the owner's idle staging buffer `rsm`), then every CTA reduces
+// and ranks its own tokens -- the whole cluster works on the top-K.
+__device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t& s_gather, int S, uint32_t split,
+                                             int t0, int nt_valid, int M, int K, const float* __restrict__ bias,
+                                             int32_t* __restrict__ ids, float* __restrict__ weights,
+                                             float* __restrict__ logits_out, long long* dbg, const EpPeers& ep,
+                                             int ntok = kRcTok) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tpc = (ntok + S - 1) / S;
+  const int my_t0 = static_cast<int>(split) * tpc;
+  const int my_rows = max(0, min(tpc, nt_valid - my_t0));
+  float* gath = reinterpret_cast<float*>(rsm);  // [S][tpc][M] (own slot unused)
+  fence_proxy_async_smem();  // generic smem accesses above before the async-proxy copies below
+  if (tid == 0 && my_rows > 0 && S > 1) mbar_arrive_expect_tx(&s_gather, static_cast<uint32_t>(my_rows * M * 4 * (S - 1)));
+  cluster_sync_all();  // partials written, barriers armed, staging buffers no longer read
+  RC_PROBE(4);
+  if (tid < S && tid != static_cast<int>(split)) {
+    const int d = tid;
+    const int rows_d = max(0, min(tpc, nt_valid - d * tpc));
+    if (rows_d > 0)
+      bulk_s2cluster(mapa_shared(gath + (static_cast<int>(split) * tpc) * M, d), part + d * tpc * M,
+                     static_cast<uint32_t>(rows_d * M * 4), mapa_shared(&s_gather, d));
+  }
+  if (my_rows > 0) {
+    if (S > 1) mbar_wait(&s_gather, 0);
+    RC_PROBE(6);
+    float* lgt = part + my_t0 * M;  // my tokens' logits, summed in place
+    for (int i = tid; i < my_rows * M; i += blockDim.x) {
+      const int r = i / M;
+      const float b = bias ? __ldg(bias + i % M) : 0.f;
+      float pv[kRcMaxSplit];
+#pragma unroll
+      for (int q = 0; q < kRcMaxSplit; ++q)
+        pv[q] = q >= S ? 0.f : (q == static_cast<int>(split) ? lgt[i] : gath[(q * tpc + r) * M + (i % M)]);
+      float acc_l = 0.f;
+#pragma unroll
+      for (int q = 0; q < kRcMaxSplit; ++q)
+        if (q < S) acc_l += pv[q];  // split order
+      if (bias) acc_l += b;
+      lgt[i] = acc_l;
+      if (logits_out) logits_out[static_cast<size_t>(t0 + my_t0) * M + i] = acc_l;
+    }
+    __syncthreads();
+    RC_PROBE(7);
+    // top-K by rank: candidate v of token r is selected at position rank(v) = #{u : l_u > l_v
+    // or (l_u == l_v and u < v)} < K -- descending, ties to the lower index (moe.py:260)
+    float* sel_v = gath;                                        // [my_rows][K] (gath slot of this CTA)
+    int* sel_i = reinterpret_cast<int*>(gath + my_rows * K);  // [my_rows][K]
+    for (int i = tid; i < my_rows * M; i += blockDim.x) {
+      const int r = i / M, v = i % M;
+      const float lv = lgt[i];
+      const float4* row = reinterpret_cast<const float4*>(lgt + r * M);
+      int rank = 0;
+      for (int u4 = 0; u4 < M / 4; ++u4) {
+        const float4 q4 = row[u4];
+        const int u = u4 * 4;
+        rank += (q4.x > lv) | ((q4.x == lv) & (u < v));
+        rank += (q4.y > lv) | ((q4.y == lv) & (u + 1 < v));
+        rank += (q4.z > lv) | ((q4.z == lv) & (u + 2 < v));
+        rank += (q4.w > lv) | ((q4.w == lv) & (u + 3 < v));
+      }
+      if (rank < K) { sel_v[r * K + rank] = lv; sel_i[r * K + rank] = v; }
+    }
+    __syncthreads();
+    for (int r = warp; r < my_rows; r += blockDim.x / 32) {  // softmax over the K picks (moe.py:261-264)
+      const float top = sel_v[r * K];
+      float den = 0.f;
+      for (int k = 0; k < K; ++k) den += __expf(sel_v[r * K + k] - top);
+      if (lane < K) {
+        const size_t o = static_cast<size_t>(t0 + my_t0 + r) * K + lane;
+        const int id = sel_i[r * K + lane];
+        const float wv = __expf(sel_v[r * K + lane] - top) / den;
+        if (ep.world == 0) {
+          ids[o] = id;
+          weights[o] = wv;
+        } else {  // expert parallel: this rank's rows of every rank's gathered table (NVLink stores)
+          const size_t og = static_cast<size_t>(ep.t0) * K + o;
+          for (int p = 0; p < ep.world; ++p) {
+            ep.ids_all[p][og] = id;
+            ep.w_all[p][og] = wv;
+          }
+        }
+      }
+    }
+  }
+  cluster_sync_relaxed();  // no CTA leaves before the copies out of its shared memory landed
+  RC_PROBE(5);
+}
+
 __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bfloat16* __restrict__ x,
                                                                    const __nv_bfloat16* __restrict__ wr,
                                                                    const float* __restrict__ bias, int T, int d_h,
@@ -255,90 +347,137 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
     }
   }
   RC_PROBE(3);
-  // exchange: the tile's tokens are spread over the cluster (CTA q owns tokens
-  // [q*tpc, (q+1)*tpc)); every CTA bulk-copies each owner its rows of this split's partial
-  // over distributed shared memory (S-1 copies per CTA, into the owner's idle staging
-  // buffer), then every CTA reduces and ranks its own tokens -- the whole cluster works
-  // on the top-K instead of one warp per token in one CTA
-  const int tpc = (kRcTok + S - 1) / S;
-  const int my_t0 = static_cast<int>(split) * tpc;
-  const int my_rows = max(0, min(tpc, nt_valid - my_t0));
-  float* gath = reinterpret_cast<float*>(rsm);  // [S][tpc][M] (own slot unused)
-  fence_proxy_async_smem();  // generic smem accesses above before the async-proxy copies below
-  if (tid == 0 && my_rows > 0 && S > 1) mbar_arrive_expect_tx(&s_gather, static_cast<uint32_t>(my_rows * M * 4 * (S - 1)));
-  cluster_sync_all();  // partials written, barriers armed, staging buffers no longer read
-  RC_PROBE(4);
-  if (tid < S && tid != static_cast<int>(split)) {
-    const int d = tid;
-    const int rows_d = max(0, min(tpc, nt_valid - d * tpc));
-    if (rows_d > 0)
-      bulk_s2cluster(mapa_shared(gath + (static_cast<int>(split) * tpc) * M, d), part + d * tpc * M,
-                     static_cast<uint32_t>(rows_d * M * 4), mapa_shared(&s_gather, d));
+  route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias, ids, weights, logits_out, dbg, ep);
+}
+
+// tcgen05 variant (default for M <= 256, K chunk a multiple of 64): the experts are the MMA's
+// M dimension (swap-AB, as in the FFN): A = this split's W_r^T chunk as [128 experts x 64 k]
+// SW128 tiles, B = the tile's 16 token rows, D = [128 experts x 16 tokens] fp32 in TMEM --
+// n_mt * kc/16 MMAs issued by one thread instead of 16 warps of mma.sync (which the profile
+// showed throughput-bound at ~4k cycles). Same split-K cluster and top-K tail.
+#ifndef SERE_ROUTE_TC
+#define SERE_ROUTE_TC 1
+#endif
+// tokens per cluster tile (MMA N). 32 measured slower (13.6 vs 11.1 us): half the CTAs, and
+// each CTA's top-K tail ranks twice the tokens
+constexpr int kRtTok = 16;
+static_assert(kRtTok == 16 || kRtTok == 32, "one or two 16-column TMEM loads per quadrant");
+constexpr int kRtTileA = 16384, kRtTileB = kRtTok * 128;
+
+struct RouteTcGeom {
+  int S, kc, nkt, n_mt;
+  size_t smem;
+};
+__host__ __device__ inline RouteTcGeom route_tc_geom(int d_h, int M) {
+  const RouteGeom g = route_geom(d_h, M);
+  RouteTcGeom t;
+  t.S = g.S;
+  t.kc = g.kc;
+  t.nkt = g.kc / 64;
+  t.n_mt = (M + 127) / 128;
+  t.smem = 1024 + static_cast<size_t>(t.n_mt) * t.nkt * kRtTileA + static_cast<size_t>(t.nkt) * kRtTileB +
+           static_cast<size_t>(kRtTok) * M * 4;
+  return t;
+}
+bool route_tc_path(int M, int K, int d_h) {
+  const RouteTcGeom t = route_tc_geom(d_h, M);
+  return SERE_ROUTE_TC && route_fast_path(M, K, d_h) && M <= 256 && t.kc % 64 == 0 && t.smem <= 200 * 1024;
+}
+
+__global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ wr,
+                                                              const float* __restrict__ bias, int T, int d_h, int M,
+                                                              int K, int kc, int32_t* __restrict__ ids,
+                                                              float* __restrict__ weights,
+                                                              float* __restrict__ logits_out, long long* dbg,
+                                                              const EpPeers ep) {
+  extern __shared__ __align__(16) uint8_t rt_raw[];
+  uint8_t* rsm = rt_raw + ((1024u - (smem_u32(rt_raw) & 1023u)) & 1023u);
+  const int nkt = kc / 64, n_mt = (M + 127) / 128;
+  uint8_t* A = rsm;                                          // [n_mt][nkt] SW128 tiles of 128 x 64
+  uint8_t* B = A + static_cast<size_t>(n_mt) * nkt * kRtTileA;  // [nkt] SW128 tiles of 16 x 64
+  float* part = reinterpret_cast<float*>(B + static_cast<size_t>(nkt) * kRtTileB);  // [kRtTok][M]
+  __shared__ __align__(8) uint64_t s_gather, s_mma;
+  __shared__ uint32_t s_tmem;
+  const int S = gridDim.y;
+  const uint32_t split = cluster_ctarank();
+  const int t0 = blockIdx.x * kRtTok, k0 = static_cast<int>(split) * kc;
+  const int kn = max(0, min(kc, d_h - k0));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nt_valid = min(kRtTok, T - t0);
+  if (tid == 0) { mbar_init(&s_gather, 1); mbar_init(&s_mma, 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(&s_tmem, 64);  // >= n_mt * kRtTok columns
+  RC_PROBE(0);
+  // stage W_r^T rows of this K chunk (static: before the PDL wait) and the token rows, 16-B
+  // cp.async into the swizzled tile positions; out-of-range chunks are zero-filled
+  // (no divisions in the issue loops: k-tile outer, 16-B chunk c = i & 7, row = i >> 3)
+  for (int kt = 0; kt < nkt; ++kt)
+    for (int i = tid; i < n_mt * 128 * 8; i += blockDim.x) {
+      const int c = i & 7, e = i >> 3, r = e & 127;
+      const int k = kt * 64 + c * 8;
+      const uint32_t avail = (e < M && k < kn) ? 16u : 0u;
+      const __nv_bfloat16* src = wr + (avail ? static_cast<size_t>(e) * d_h + k0 + k : 0);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                       smem_u32(A + ((e >> 7) * nkt + kt) * kRtTileA + r * 128 + ((c ^ (r & 7)) << 4))),
+                   "l"(src), "r"(avail)
+                   : "memory");
+    }
+  RC_PROBE(1);
+  pdl_wait();  // x = the previous layer's RMSNorm output; ids/weights are read by its kernels
+  pdl_trigger();
+  for (int i = tid; i < kRtTok * nkt * 8; i += blockDim.x) {
+    const int c = i & 7, r = (i >> 3) & (kRtTok - 1), kt = i / (kRtTok * 8);  // (constant divisor)
+    const int k = kt * 64 + c * 8;
+    const uint32_t avail = (r < nt_valid && k < kn) ? 16u : 0u;
+    const __nv_bfloat16* src = x + (avail ? static_cast<size_t>(t0 + r) * d_h + k0 + k : 0);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                     smem_u32(B + kt * kRtTileB + r * 128 + ((c ^ (r & 7)) << 4))),
+                 "l"(src), "r"(avail)
+                 : "memory");
   }
-  if (my_rows > 0) {
-    if (S > 1) mbar_wait(&s_gather, 0);
-    RC_PROBE(6);
-    float* lgt = part + my_t0 * M;  // my tokens' logits, summed in place
-    for (int i = tid; i < my_rows * M; i += blockDim.x) {
-      const int r = i / M;
-      const float b = bias ? __ldg(bias + i % M) : 0.f;
-      float pv[kRcMaxSplit];
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  fence_proxy_async_shared_cta();  // generic (cp.async) smem writes -> async-proxy MMA reads
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  RC_PROBE(2);
+  const uint32_t tmem = s_tmem;
+  if (tid == 0) {
+    const uint32_t idesc = umma_idesc_bf16(128, kRtTok);
+    for (int mt = 0; mt < n_mt; ++mt)
+      for (int kt = 0; kt < nkt; ++kt) {
+        const uint32_t a = smem_u32(A + (mt * nkt + kt) * kRtTileA), b = smem_u32(B + kt * kRtTileB);
 #pragma unroll
-      for (int q = 0; q < kRcMaxSplit; ++q)
-        pv[q] = q >= S ? 0.f : (q == static_cast<int>(split) ? lgt[i] : gath[(q * tpc + r) * M + (i % M)]);
-      float acc_l = 0.f;
-#pragma unroll
-      for (int q = 0; q < kRcMaxSplit; ++q)
-        if (q < S) acc_l += pv[q];  // split order
-      if (bias) acc_l += b;
-      lgt[i] = acc_l;
-      if (logits_out) logits_out[static_cast<size_t>(t0 + my_t0) * M + i] = acc_l;
-    }
-    __syncthreads();
-    RC_PROBE(7);
-    // top-K by rank: candidate v of token r is selected at position rank(v) = #{u : l_u > l_v
-    // or (l_u == l_v and u < v)} < K -- descending, ties to the lower index (moe.py:260)
-    float* sel_v = gath;                                        // [my_rows][K] (gath slot of this CTA)
-    int* sel_i = reinterpret_cast<int*>(gath + my_rows * K);  // [my_rows][K]
-    for (int i = tid; i < my_rows * M; i += blockDim.x) {
-      const int r = i / M, v = i % M;
-      const float lv = lgt[i];
-      const float4* row = reinterpret_cast<const float4*>(lgt + r * M);
-      int rank = 0;
-      for (int u4 = 0; u4 < M / 4; ++u4) {
-        const float4 q4 = row[u4];
-        const int u = u4 * 4;
-        rank += (q4.x > lv) | ((q4.x == lv) & (u < v));
-        rank += (q4.y > lv) | ((q4.y == lv) & (u + 1 < v));
-        rank += (q4.z > lv) | ((q4.z == lv) & (u + 2 < v));
-        rank += (q4.w > lv) | ((q4.w == lv) & (u + 3 < v));
+        for (int k16 = 0; k16 < 4; ++k16)
+          umma_bf16(tmem + mt * kRtTok, umma_desc_sw128(a + 32 * k16), umma_desc_sw128(b + 32 * k16), idesc,
+                    (kt | k16) ? 1u : 0u);
       }
-      if (rank < K) { sel_v[r * K + rank] = lv; sel_i[r * K + rank] = v; }
-    }
-    __syncthreads();
-    for (int r = warp; r < my_rows; r += blockDim.x / 32) {  // softmax over the K picks (moe.py:261-264)
-      const float top = sel_v[r * K];
-      float den = 0.f;
-      for (int k = 0; k < K; ++k) den += __expf(sel_v[r * K + k] - top);
-      if (lane < K) {
-        const size_t o = static_cast<size_t>(t0 + my_t0 + r) * K + lane;
-        const int id = sel_i[r * K + lane];
-        const float wv = __expf(sel_v[r * K + lane] - top) / den;
-        if (ep.world == 0) {
-          ids[o] = id;
-          weights[o] = wv;
-        } else {  // expert parallel: this rank's rows of every rank's gathered table (NVLink stores)
-          const size_t og = static_cast<size_t>(ep.t0) * K + o;
-          for (int p = 0; p < ep.world; ++p) {
-            ep.ids_all[p][og] = id;
-            ep.w_all[p][og] = wv;
-          }
-        }
+    umma_commit(&s_mma);
+  }
+  mbar_wait(&s_mma, 0);
+  tc_fence_after();
+  if (warp < 4 * (kRtTok / 16)) {  // TMEM lane quadrant = warp & 3: experts mt*128 + 32*(warp&3) +
+                                    // lane; warps 4-7 take token columns 16-31 when kRtTok = 32
+    const int q = warp & 3, c0 = (warp >> 2) * 16;
+    for (int mt = 0; mt < n_mt; ++mt) {
+      uint32_t v[16];
+      tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + mt * kRtTok + c0, v);
+      tmem_wait_ld();
+      const int e = mt * 128 + q * 32 + lane;
+      if (e < M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) part[(c0 + j) * M + e] = __uint_as_float(v[j]);
       }
     }
   }
-  cluster_sync_relaxed();  // no CTA leaves before the copies out of its shared memory landed
-  RC_PROBE(5);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 64);
+  }
+  RC_PROBE(3);
+  route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias, ids, weights, logits_out, dbg, ep, kRtTok);
 }
 
 size_t route_workspace_bytes(int T, int d_h, int M) { return 256; }
@@ -352,6 +491,33 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
                              cudaStream_t stream, const EpPeers* ep) {
   (void)ws;
   if (T <= 0) return cudaSuccess;
+  if (route_tc_path(M, K, d_h)) {
+    const RouteTcGeom g = route_tc_geom(d_h, M);
+    static size_t configured_tc = 0;
+    if (g.smem > 48 * 1024 && g.smem > configured_tc) {
+      cudaError_t e = cudaFuncSetAttribute(route_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(g.smem));
+      if (e != cudaSuccess) return e;
+      configured_tc = g.smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((T + kRtTok - 1) / kRtTok, g.S, 1);
+    cfg.blockDim = dim3(kRcThreads, 1, 1);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = g.S;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 2 : 1;
+    EpPeers none{};
+    return cudaLaunchKernelEx(&cfg, route_tc_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
+                              logits_out, g_route_dbg, ep ? *ep : none);
+  }
   const RouteGeom g = route_geom(d_h, M);
   static size_t configured = 0;
   if (g.smem > 48 * 1024 && g.smem > configured) {
