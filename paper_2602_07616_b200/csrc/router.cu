@@ -358,6 +358,12 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
 #ifndef SERE_ROUTE_TC
 #define SERE_ROUTE_TC 1
 #endif
+// 1: the tcgen05 router launches with programmatic dependent launch, so its CTAs stage the
+// static router weights while the previous kernel (combine) finishes; its outputs are
+// written after griddepcontrol.wait. -1% step time (24-layer trace, 2 reps)
+#ifndef SERE_PDL_ROUTER
+#define SERE_PDL_ROUTER 1
+#endif
 // tokens per cluster tile (MMA N). 32 measured slower (13.6 vs 11.1 us): half the CTAs, and
 // each CTA's top-K tail ranks twice the tokens
 constexpr int kRtTok = 16;
@@ -513,7 +519,7 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = g_pdl ? 2 : 1;
+    cfg.numAttrs = (g_pdl || SERE_PDL_ROUTER) ? 2 : 1;
     EpPeers none{};
     return cudaLaunchKernelEx(&cfg, route_tc_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
                               logits_out, g_route_dbg, ep ? *ep : none);
