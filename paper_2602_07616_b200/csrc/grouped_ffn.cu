@@ -665,7 +665,10 @@ cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream)
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  return launch_pdl(g_pdl, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
+#ifndef SERE_PDL_FFN
+#define SERE_PDL_FFN 0
+#endif
+  return launch_pdl(g_pdl || SERE_PDL_FFN, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
 }
 
 size_t moe_ffn_smem(int Et) { return ffn_smem_bytes(Et); }
