@@ -54,7 +54,8 @@ def test_host_side_functions(lib):
     # bank bytes = E * 3 * d_h_pad * d_m_pad * 2 (bf16)
     assert lib.sere_expert_bank_bytes(128, 2048, 768) == 128 * 3 * 2048 * 768 * 2
     assert lib.sere_expert_bank_bytes(8, 4096, 14336) == 8 * 3 * 4096 * 14336 * 2
-    # d_h, d_m padded to 128; the single down m-tile is stored as a (zero-padded) m-tile pair
+    # d_h, d_m padded to 128; the single down m-tile is stored in a (zero-padded) group of
+    # kW2Group = SERE_MW_DN_MAX = 2 m-tiles (a down unit reads its m-tiles with one copy)
     assert lib.sere_expert_bank_bytes(5, 24, 40) == 5 * (2 * 128 * 128 + 2 * 128 * 128) * 2
     L = _lib.workspace_layout(512, 8, 128, 0, 2048, 768)
     assert L.r_max >= 512 * 8 + 16 * 128 and L.r_max % 8 == 0
