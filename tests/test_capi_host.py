@@ -139,3 +139,39 @@ def test_ep_peers_struct_matches_c_header(tmp_path):
     vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert vals[0] == ctypes.sizeof(_lib.EpPeers)
     assert vals[1:] == [getattr(_lib.EpPeers, f).offset for f in fields]
+
+
+def test_ep_peers_host_wiring():
+    """P2PDecodeStep._build_peers (host logic, no GPU): expert blocks, shared ownership and
+    every rank's workspace pointers land in the right `sere_ep_peers` slots."""
+    import types
+
+    from paper_2602_07616_b200 import _lib, ep
+    from paper_2602_07616_b200.ep_p2p import P2PDecodeStep
+
+    class _T:
+        def __init__(self, p):
+            self.p = p
+
+        def data_ptr(self):
+            return self.p
+
+    world, M, K, d_h, d_m, T, n_sh = 4, 30, 4, 256, 128, 64, 3
+    st = P2PDecodeStep.__new__(P2PDecodeStep)
+    st.model = types.SimpleNamespace(M=M, K=K, d_h=d_h, d_m=d_m)
+    st.world, st.rank, st.T, st.n_shared_total = world, 1, T, n_sh
+    st.t0 = 16
+    regions = [types.SimpleNamespace(ws_ptr=(r + 1) << 32, h_all=_T(0x1000 + r), ids_all=_T(0x2000 + r),
+                                     w_all=_T(0x3000 + r), flags=_T(0x4000 + r)) for r in range(world)]
+    st._build_peers(regions)
+    p = st.peers
+    assert (p.world, p.rank, p.t0, p.T_all) == (world, 1, 16, T)
+    assert [p.e_lo[r] for r in range(world + 1)] == [ep.expert_range(M, world, r)[0] for r in range(world)] + [M]
+    assert [p.nsh[r] for r in range(world)] == [len(ep.shared_owned(n_sh, world, r)) for r in range(world)]
+    for r in range(world):
+        lo, hi = ep.expert_range(M, world, r)
+        L = _lib.workspace_layout(T, K, hi - lo, p.nsh[r], d_h, d_m)
+        assert p.r_max[r] == L.r_max
+        assert p.y_perm[r] == regions[r].ws_ptr + L.off_y_perm
+        assert p.slot_row[r] == regions[r].ws_ptr + L.off_slot_row
+        assert (p.h_all[r], p.ids_all[r], p.w_all[r], p.flags[r]) == (0x1000 + r, 0x2000 + r, 0x3000 + r, 0x4000 + r)
