@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
             else for (int q = 0; q < 4 && f0 + q < d_h; ++q) hd[q] = __float2bfloat16_rn(hv[q]);
           }
         }
+        if (ep.world) __threadfence_system();  // peer stores visible before the next barrier
         return;
       }
       for (int b2 = 0; b2 < d_h; b2 += blockDim.x * kRowVec)
@@ -363,6 +364,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
                         : h_next + static_cast<size_t>(t) * d_h)[f0 + q] = __float2bfloat16_rn(hv);
           }
         }
+      if (ep.world) __threadfence_system();
       return;
     }
   }

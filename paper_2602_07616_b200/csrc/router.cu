@@ -245,6 +245,7 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
             ep.ids_all[p][og] = id;
             ep.w_all[p][og] = wv;
           }
+          __threadfence_system();  // peer stores visible before the barrier kernel's release
         }
       }
     }
