@@ -235,6 +235,18 @@ def algorithmic_bytes(wl, n_active, T):
             + 8 * T * wl["K"])
 
 
+def workload_config(args, wl, world):
+    """The `config` object of both arms (identical for --impl ours and --impl reference)."""
+    w_bytes = 2 * 3 * wl["d_h"] * wl["d_m"] * (wl["M"] + wl["n_shared"]) * wl["L"]
+    return {"workload": wl["name"], "global_batch": wl["T"], "layers": wl["L"], "experts": wl["M"],
+            "top_k": wl["K"], "d_h": wl["d_h"], "d_m": wl["d_m"], "shared_experts": wl["n_shared"],
+            "retain_S": args.retain, "threshold_rho": args.threshold, "router_skew_beta": args.beta,
+            "sim": args.sim, "block": "prenorm_residual (RMSNorm -> router -> SERE -> grouped FFN -> +x)",
+            "parallelism": f"ep{world}",
+            "l2": f"no flush: {w_bytes / 1e9:.2f} GB of expert weights per step vs 126 MB L2"
+                  + ("" if w_bytes > 4 * 126e6 else " (single-layer config: the FFN replay line flushes L2)")}
+
+
 # --------------------------------------------------------------------------- CPU baseline
 def cpu_layer_sample(wl, layer_np, h, sim, S, rho, bias, seconds):
     """Time the reference per-layer body (fp64) on one layer: route + apply_sere + layer_forward."""
@@ -242,11 +254,12 @@ def cpu_layer_sample(wl, layer_np, h, sim, S, rho, bias, seconds):
 
     from oracle import sere_oracle as O
 
-    def once():
-        logits = h @ layer_np.w_router + bias[None, :]
+    def once():  # the benchmarked block body (decode.DecodeStep, prenorm_residual) in fp64
+        hb = O.bf16_round(O.rms_norm(h))
+        logits = hb @ layer_np.w_router + bias[None, :]
         ids, w = O.topk_softmax(logits, wl["K"])
         res = O.apply_sere(ids, sim, S, rho)
-        return O.layer_forward(layer_np, h, res.new_indices, w)
+        return h + O.layer_forward(layer_np, hb, res.new_indices, w)
 
     once()  # numpy / BLAS warm-up
     times = []
@@ -256,6 +269,33 @@ def cpu_layer_sample(wl, layer_np, h, sim, S, rho, bias, seconds):
         once()
         times.append(time.perf_counter() - t0)
     return float(np.median(times)), len(times)
+
+
+def cpu_apply_sere_us(model, retain, threshold, Ts=(64, 512), runs=7):
+    """rerouting.apply_sere alone (the oracle port, bit-identical to the reference)
+    on the host, median of `runs` after one warm-up, on the same router/sim as the device
+    `reroute_only_us` figure (layer 0, T tokens from a seeded N(0,1) batch)."""
+    import numpy as np
+
+    from oracle import sere_oracle as O
+
+    layer = model.layers[0]
+    w_r = layer.w_router.double().cpu().numpy()
+    bias = layer.bias.double().cpu().numpy()
+    sim = model.sims_host[0]
+    out = {}
+    for T in Ts:
+        x = O.bf16_round(np.random.default_rng(T).standard_normal((T, w_r.shape[0])))
+        ids, _ = O.topk_softmax(x @ w_r + bias[None, :], model.K)
+        O.apply_sere(ids, sim, retain, threshold)
+        ts = []
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            O.apply_sere(ids, sim, retain, threshold)
+            ts.append(time.perf_counter() - t0)
+        out[f"T={T}"] = round(float(np.median(ts)) * 1e6, 1)
+    out["note"] = f"oracle apply_sere (rerouting.py:130-171 restated), 1 host thread, median of {runs}"
+    return out
 
 
 def time_reroute_only(torch, model, retain, threshold, Ts=(64, 512), reps=50):
@@ -418,14 +458,18 @@ def run_ours(args, wl):
     act_sere = sere.active_counts().astype(float)
     act_topk = topk.active_counts().astype(float)
 
-    # ---- roofline pass: the same SERE step with per-stage CUDA events captured in its graph
-    prof = make_step("sere")
-    prof.x_in.copy_(x_local)
-    prof.enable_stage_events()
-    roof = None
-    reroute_us = None
-    stage_mode = "cuda-graph event-record nodes"
-    if getattr(prof, "stage_events", None) is not None:
+    # ---- roofline pass: the same SERE (and top-k) step with per-stage CUDA events captured in its graph
+    n_sh_local = len(model.shared_ids)
+    wl_local = dict(wl, n_shared=n_sh_local)
+    peak, peak_kind = measured_peak_hbm()
+
+    def stage_pass(mode):
+        prof = make_step(mode)
+        prof.x_in.copy_(x_local)
+        prof.enable_stage_events()
+        if getattr(prof, "stage_events", None) is None:
+            return None
+        stage_mode = "cuda-graph event-record nodes"
         prof.capture()
         for _ in range(3):
             prof.run()
@@ -440,32 +484,41 @@ def run_ours(args, wl):
                 prof.run()
             torch.cuda.synchronize()
             st = prof.stage_times_ms()
-        acts = prof.active_counts()
         if world > 1:
             cls = [o.reroute.expert_class[lo:hi].cpu().numpy() for o in prof.outs]
             acts_local = np.array([int(((c & 3) != 0).sum()) for c in cls], dtype=float)
         else:
-            acts_local = acts.astype(float)
+            acts_local = prof.active_counts().astype(float)
+        del prof
         ffn_ms = st[:, 2] + st[:, 3]
-        n_sh_local = len(model.shared_ids)
-        wl_local = dict(wl, n_shared=n_sh_local)
         bytes_layers = np.array([algorithmic_bytes(wl_local, a, T) for a in acts_local], dtype=float)
         achieved = float(bytes_layers.sum() / (ffn_ms.sum() * 1e-3) / 1e9)
-        peak, peak_kind = measured_peak_hbm()
-        traffic, traffic_src = ncu_traffic()
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "moe_ffn_kernel (gate/up + down phases in one persistent tcgen05 launch)",
-                "peak_kind": peak_kind,
-                "bytes_per_layer_avg": float(bytes_layers.mean()),
-                "ffn_us_per_layer_avg": float(ffn_ms.mean() * 1e3),
-                "stage_us_per_layer_avg": {k: round(float(v) * 1e3, 2) for k, v in
+        return {"stage_us_per_layer_avg": {k: round(float(v) * 1e3, 2) for k, v in
                                            zip(["reroute_align", "permute", "ffn", "unused", "combine"],
                                                st.mean(axis=0))},
+                "ffn_achieved_gbs": round(achieved, 1), "ffn_frac": round(achieved / peak, 4),
+                "ffn_bytes_per_layer_avg": float(bytes_layers.mean()),
+                "ffn_us_per_layer_avg": round(float(ffn_ms.mean() * 1e3), 2),
                 "ffn_share_of_layer_kernels": round(float(ffn_ms.sum() / st.sum()), 4),
-                "timing": f"CUDA events per stage, {stage_mode}, last of 3 steps"}
-        reroute_us = round(float(st[:, 0].mean() * 1e3), 2)
-        del prof
+                "timing": f"CUDA events per stage, {stage_mode}, last of 3 steps (includes ~2.7 us of "
+                          "event-node overhead per stage)"}
+
+    sp_sere = stage_pass("sere")
+    sp_topk = stage_pass("topk")
+    roof = None
+    reroute_us = None
+    if sp_sere is not None:
+        traffic, traffic_src = ncu_traffic()
+        roof = {"bound": "hbm", "achieved": sp_sere["ffn_achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": sp_sere["ffn_frac"], "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "moe_ffn_kernel (gate/up + down phases in one persistent tcgen05 launch)",
+                "peak_kind": peak_kind,
+                "bytes_per_layer_avg": sp_sere["ffn_bytes_per_layer_avg"],
+                "ffn_us_per_layer_avg": sp_sere["ffn_us_per_layer_avg"],
+                "stage_us_per_layer_avg": sp_sere["stage_us_per_layer_avg"],
+                "ffn_share_of_layer_kernels": sp_sere["ffn_share_of_layer_kernels"],
+                "timing": sp_sere["timing"]}
+        reroute_us = sp_sere["stage_us_per_layer_avg"]["reroute_align"]
     reroute_only = None
     if world == 1:
         try:
@@ -483,11 +536,7 @@ def run_ours(args, wl):
         sere.run()
         torch.cuda.synchronize()
         bank = model.layers[-1].bank
-        if hasattr(sere, "workspace"):  # peer-memory EP: the workspace lives in the rank's peer region
-            ws_ptr, ws_bytes = sere.workspace
-        else:
-            ws = _moe_mod.workspace(T, wl["K"], bank.M, bank.n_shared, wl["d_h"], wl["d_m"], bank.device)
-            ws_ptr, ws_bytes = ws.data_ptr(), ws.numel()
+        ws_ptr, ws_bytes = sere.workspace  # the step's own workspace (peer region under P2P EP)
         stream = torch.cuda.current_stream()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         lib.call("sere_debug_replay_ffn", bank.data.data_ptr(), bank.M, bank.n_shared, wl["d_h"], wl["d_m"], 0, T,
@@ -514,7 +563,7 @@ def run_ours(args, wl):
         roof["kernel_bytes"] = b_last
         roof["timing"] = (f"achieved/frac: CUDA events around {reps} back-to-back moe_ffn_kernel launches on the "
                           f"last layer's plan ({int(act_last)} active experts, sere_debug_replay_ffn); "
-                          f"*_stage_events: " + roof["timing"] + " (includes ~2.7 us of event-node overhead)")
+                          f"*_stage_events: " + roof["timing"])
     clocks.close()
 
     # ---- CPU baseline: rank 0, N = 1 only
@@ -529,9 +578,11 @@ def run_ours(args, wl):
             t_layer, n = cpu_layer_sample(wl, layer_np, h0, sim0, args.retain, args.threshold, bias0,
                                           args.cpu_seconds)
             cpu = {"value": round(T / (t_layer * L), 3), "unit": "tokens/s", "cores": blas, "kind": "port",
-                   "sample": f"1 of {L} layers (fp64 route_topk + apply_sere + layer_forward, T={T}), "
-                             f"median of {n} runs = {t_layer * 1e3:.1f} ms, extrapolated x{L}",
-                   "cpu_model": cpu_model, "host_cores": cores}
+                   "sample": f"1 of {L} layers (fp64 prenorm block: RMSNorm + route_topk + apply_sere + "
+                             f"layer_forward + residual, T={T}), median of {n} runs = {t_layer * 1e3:.1f} ms, "
+                             f"extrapolated x{L}",
+                   "cpu_model": cpu_model, "host_cores": cores, "blas_threads": blas,
+                   "apply_sere_us": cpu_apply_sere_us(model, args.retain, args.threshold)}
             del layer_np
         except MemoryError as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "port", "sample": f"skipped: {exc}"}
@@ -552,14 +603,10 @@ def run_ours(args, wl):
         "dtype": "bf16",
         "data": "synthetic: random N(0,1/d_h) bf16 expert/router weights, N(0,1) token states, "
                 "uniform symmetric similarity (reference test construction), router skew beta",
-        "config": {"workload": wl["name"], "global_batch": T, "layers": L, "experts": wl["M"], "top_k": wl["K"],
-                   "d_h": wl["d_h"], "d_m": wl["d_m"], "shared_experts": wl["n_shared"],
-                   "retain_S": args.retain, "threshold_rho": args.threshold, "router_skew_beta": args.beta,
-                   "sim": args.sim, "block": "prenorm_residual (RMSNorm -> router -> SERE -> grouped FFN -> +x)",
-                   "parallelism": f"ep{world}", "ep_transport": transport, "l2": "no flush: 58 GB of expert weights per step >> 126 MB L2",
-                   "cuda_graph": all(graphed)},
+        "config": workload_config(args, wl, world),
         "topk": {"value": round(tok_s_topk, 1), "unit": "tokens/s", "ms_per_step": round(ms_topk, 4),
-                 "active_experts_per_layer": round(float(act_topk.mean()), 2)},
+                 "active_experts_per_layer": round(float(act_topk.mean()), 2),
+                 "stages": sp_topk},
         "sere": {"active_experts_per_layer": round(float(act_sere.mean()), 2),
                  "weight_bytes_skipped_frac": round(1.0 - float(act_sere.sum() / max(act_topk.sum(), 1)), 4),
                  "speedup_vs_topk": round(ms_topk / ms_sere, 4)},
@@ -568,6 +615,8 @@ def run_ours(args, wl):
         "reroute_only_us": reroute_only,
         "roofline": roof,
         "cpu_baseline": cpu,
+        "ep_transport": transport,
+        "cuda_graph": all(graphed),
         "e2e": {"value": round(T / (ms_e2e * 1e-3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),
                 "ms_per_step": round(ms_e2e, 4)},
@@ -606,13 +655,13 @@ def run_reference(args, wl):
     bias = args.beta * rng.standard_normal(M)
     sim = clustered_sim(rng, M) if args.sim == "clustered" else uniform_sim(rng, M)
     x = rng.standard_normal((T, d_h))
-    h = x / np.sqrt((x * x).mean(axis=1, keepdims=True) + 1e-6)
 
-    def sample():
+    def sample():  # one layer of the benchmarked block (decode.DecodeStep, prenorm_residual), fp64
+        h = O.bf16_round(O.rms_norm(x))
         logits = h @ layer.w_router + bias[None, :]
         ids, w = O.topk_softmax(logits, K)
         res = O.apply_sere(ids, sim, args.retain, args.threshold)
-        return O.layer_forward(layer, h, res.new_indices, w)
+        return x + O.layer_forward(layer, h, res.new_indices, w)
 
     for _ in range(args.warmup):
         sample()
@@ -620,21 +669,23 @@ def run_reference(args, wl):
     for _ in range(args.steps):
         sample()
     t_layer = (time.perf_counter() - t0) / args.steps
-    ms_step = t_layer * L * 1e3
-    value = T / (ms_step * 1e-3)
+    value = T / (t_layer * L)
     cores, cpu_model, blas = host_info()
     line = {
         "impl": "reference",
         "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup,
+        # each timed step is ONE layer of the L-layer decode step (a bounded sample: an fp64 step
+        # of all L layers needs L x 4.8 GB of weights); value = T / (L x ms_per_step)
+        "ms_per_step": round(t_layer * 1e3, 3),
+        "ms_per_decode_step_extrapolated": round(t_layer * L * 1e3, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic, same shapes/distributions as the ours arm",
-        "config": {"workload": wl["name"], "global_batch": T, "layers": L, "experts": M, "top_k": K, "d_h": d_h,
-                   "d_m": d_m, "shared_experts": ns, "retain_S": args.retain, "threshold_rho": args.threshold,
-                   "router_skew_beta": args.beta, "sim": args.sim, "parallelism": "cpu"},
+        "config": workload_config(args, wl, world),
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": blas, "kind": "port",
                          "sample": f"each step = 1 of {L} layers (fp64 oracle port of the reference per-layer "
-                                   f"body), extrapolated x{L}", "cpu_model": cpu_model, "host_cores": cores},
+                                   f"body in the prenorm block), value extrapolated x{L}",
+                         "cpu_model": cpu_model, "host_cores": cores, "blas_threads": blas},
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -57,13 +57,20 @@ enum {
   SERE_CLASS_REROUTED = 4  /* secondary redirected; target in reroute_map[e]    rerouting.py:162-164 */
 };
 
+/* Expert id the router writes for a token whose logits are not all finite (a non-finite
+ * token state; the reference's route_topk raises DomainError, moe.py:274-275). The
+ * re-routing / align kernels report it as SERE_ERR_DOMAIN. */
+#define SERE_ID_NONFINITE ((int32_t)0x80000000)
+
 /* activations of moe.py:22 */
 enum { SERE_ACT_SILU = 0, SERE_ACT_RELU = 1, SERE_ACT_GELU_TANH = 2 };
 
 /* flags for sere_reroute / sere_moe_forward */
 enum {
   SERE_FLAG_CHECK_SIM = 1 /* validate sim in [0,1] on the device (InputError); the Python
-                             mirror validates once per uploaded matrix instead */
+                             drop-in (apply_sere) sets it on every call, as the reference
+                             validates on every call (rerouting.py:140); the device-level
+                             API validates once per uploaded DeviceSimilarity */
 };
 
 int sere_abi_version(void);
@@ -231,7 +238,8 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
  *     all-gather / reduce-scatter choreography of (4b) -- the reference has no
  *     multi-GPU path, so these have no reference counterpart beyond moe.py:280-310).
  *     Each rank owns: gathered token states h_all bf16 [T_all,d_h], router ids_all
- *     i32 [T_all,K] and w_all f32 [T_all,K], barrier flags i32 [world] (zeroed once),
+ *     i32 [T_all,K] and w_all f32 [T_all,K], barrier flags i32 [SERE_MAX_EP_RANKS + 1]
+ *     (zeroed once; the last word is the rank's sticky abort word),
  *     and its layer workspace (y_perm / slot_row inside it, sere_layer_workspace_layout).
  *     All of them must be reachable from every rank (cudaIpcOpenMemHandle, see
  *     sere_ipc_*); sere_ep_peers lists every rank's pointers, entry `rank` = own.
@@ -259,7 +267,10 @@ int sere_route_topk_ep(const sere_ep_peers* peers, const uint16_t* x_local, cons
                        const float* bias, int T_local, int d_h, int M, int K, void* workspace,
                        size_t workspace_bytes, void* stream);
 /* Flag barrier over the group (one warp). epoch_dev: this rank's device counter (zeroed
- * once). On a wait longer than timeout_ns: SERE_ERR_CUDA in status_dev, no hang. */
+ * once). On a wait longer than timeout_ns: SERE_ERR_CUDA in status_dev, no hang, and the
+ * abort word of EVERY rank is set: from then on every rank's barriers fail fast and its
+ * router / combine skip their peer stores and loads (the step's outputs are invalid and
+ * each rank's status says so). */
 int sere_ep_barrier(const sere_ep_peers* peers, int32_t* epoch_dev, int32_t* status_dev, int64_t timeout_ns,
                     void* stream);
 /* (4b) without its combine: re-route + align + permute + fused FFN of this rank's experts

@@ -283,6 +283,51 @@ def model_forward(layers, x, activation="silu", retain_count=None, threshold=Non
     return x, traces
 
 
+def bf16_round(a) -> np.ndarray:
+    """Round to bfloat16 (nearest-even, via float32) and widen back to float64: the values a
+    bf16 tensor holds. Used to hand the oracle exactly what the device computes on."""
+    f = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64)
+
+
+def rms_norm(x: np.ndarray, eps: float = 1e-6) -> np.ndarray:
+    """x / sqrt(mean(x^2) + eps) per row (no gain): the pre-norm of the benchmark block."""
+    x = np.asarray(x, dtype=np.float64)
+    return x / np.sqrt((x * x).mean(axis=1, keepdims=True) + eps)
+
+
+def block_forward(layers, x0, sims, retain_count, threshold, routes, eps: float = 1e-6,
+                  activation: str = "silu"):
+    """The pre-norm residual decode block the benchmark runs (decode.DecodeStep, block=
+    "prenorm_residual"): per layer
+
+        h = bf16(RMSNorm(x));  ids, w = routes[l];  ids' = apply_sere(ids, sims[l], S, rho)
+        x = x + layer_forward(layer, h, ids', w)                    (moe.py:280-310, 362-375)
+
+    The reference chains raw outputs (x <- layer_forward(x), moe.py:375); the block adds the
+    residual stream and the RMSNorm around the same two reference operators. `routes[l]` are
+    the router's (ids, weights) of layer l, teacher-forced from the device router exactly as
+    `model_forward`'s router_override does (moe.py:334,363-364). `retain_count=None` skips
+    the rewrite (plain top-k). Returns (x, traces) with traces[l] = dict(x, h, final, active).
+    """
+    x = np.asarray(x0, dtype=np.float64)
+    traces = []
+    for l, layer in enumerate(layers):
+        h = bf16_round(rms_norm(x, eps))
+        ids, w = routes[l]
+        if retain_count is not None:
+            res = apply_sere(ids, sims[l], retain_count, threshold)
+            final, active = res.new_indices, res.final_active
+        else:
+            final = np.asarray(ids, dtype=np.int64)
+            active = frozenset(np.unique(final).tolist())
+        traces.append(dict(x=x, h=h, final=final, active=active))
+        x = x + layer_forward(layer, h, final, w, activation)
+    return x, traces
+
+
 def gen_layers(seed: int, n_layers: int, n_experts: int, top_k: int, d_h: int, d_m: int,
                n_shared: int = 0) -> list:
     """moe.py:380-421 (`gen_model`): identical draw order, so the same seed gives the same tensors."""

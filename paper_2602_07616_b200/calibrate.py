@@ -50,9 +50,9 @@ def _act(kind: str):
         return torch.nn.functional.silu
     if kind == "relu":
         return torch.relu
-    if kind == "gelu_tanh":
+    if kind == "gelu-tanh":  # the reference's spelling (moe.py:22,42-45; moe.ACTIVATIONS)
         return lambda g: torch.nn.functional.gelu(g, approximate="tanh")
-    raise ConfigError(f"unknown activation {kind!r}")
+    raise ConfigError(f"unknown activation {kind!r}, expected one of {_moe.ACTIVATIONS}")
 
 
 def _pair_scores(y, metric: str) -> np.ndarray:

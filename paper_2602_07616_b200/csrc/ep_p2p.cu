@@ -13,7 +13,8 @@
 // flag array (release, system scope) and waits until all of its own slots reach i
 // (acquire). Epochs come from a device counter, so a CUDA graph of the step can be
 // replayed. A barrier that waits longer than `timeout_ns` sets SERE_ERR_CUDA in the
-// status word and returns instead of hanging the device.
+// status word, raises the sticky abort word of every rank (params.cuh kEpAbortSlot) and
+// returns instead of hanging the device.
 #include <cuda_runtime.h>
 
 #include "../../include/sere_b200.h"
@@ -22,24 +23,20 @@
 
 namespace sere {
 
-__device__ __forceinline__ void st_release_sys(int32_t* p, int v) {
-  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __global__ void __launch_bounds__(32) ep_barrier_kernel(const EpPeers ep, int32_t* epoch, int32_t* status,
                                                          long long timeout_ns) {
-  __shared__ int s_epoch;
+  __shared__ int s_epoch, s_abort;
   const int lane = threadIdx.x;
   if (lane == 0) {
     s_epoch = *epoch + 1;
     *epoch = s_epoch;
+    s_abort = ep_aborted(ep);
   }
   __syncwarp();
+  if (s_abort) {  // an earlier barrier of some rank timed out: fail fast, never wait
+    if (lane == 0 && status) atomicExch(status, SERE_ERR_CUDA);
+    return;
+  }
   const int e = s_epoch;
   // the stream's earlier kernels (router / FFN) are complete; make their peer stores visible
   // system-wide before announcing the arrival
@@ -51,6 +48,9 @@ __global__ void __launch_bounds__(32) ep_barrier_kernel(const EpPeers ep, int32_
       __nanosleep(100);
       if (globaltimer_ns() - t0 > static_cast<unsigned long long>(timeout_ns)) {
         if (status) atomicExch(status, SERE_ERR_CUDA);
+        // sticky and visible to every rank: their next barrier fails fast and their peer
+        // kernels skip the exchange (a late peer must not pass on this rank's newer epochs)
+        for (int p = 0; p < ep.world; ++p) st_release_sys(ep.flags[p] + kEpAbortSlot, 1);
         break;
       }
     }

@@ -672,13 +672,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
 
 cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream) {
   const size_t smem = ffn_smem_bytes(p.Et);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(moe_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static SmemAttrCache attr;
+  if (cudaError_t e = ensure_smem_attr(moe_ffn_kernel, smem, attr, 0); e != cudaSuccess) return e;
 #ifndef SERE_PDL_FFN
 #define SERE_PDL_FFN 0
 #endif

@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
     }
   } else {
     pdl_wait();  // peers' slot rows are ordered by the barrier kernel before us: wait for it
+    if (ep_aborted(ep)) return;  // a barrier timed out: no peer loads or stores on this step
     const int tg = ep.t0 + t, TK = ep.T_all * K;
     for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
       int o, idx;

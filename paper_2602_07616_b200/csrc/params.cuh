@@ -78,6 +78,24 @@ inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+// The max-dynamic-shared-memory attribute is per device: each launcher keeps the largest
+// size it has set for every device (a second GPU in the same process sets its own).
+constexpr int kMaxDevices = 64;
+struct SmemAttrCache {
+  size_t configured[kMaxDevices] = {};
+};
+template <typename Kernel>
+inline cudaError_t ensure_smem_attr(Kernel kernel, size_t smem, SmemAttrCache& cache, size_t default_cap = 48 * 1024) {
+  if (smem <= default_cap) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < kMaxDevices && cache.configured[dev] >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess && dev >= 0 && dev < kMaxDevices) cache.configured[dev] = smem;
+  return e;
+}
+
 // Expert-parallel group seen through NVLink peer memory (ep_p2p.cu; world == 0: single GPU).
 // Every pointer array is indexed by rank; entry `rank` is this rank's own buffer.
 constexpr int kMaxEpRanks = 8;
@@ -94,6 +112,24 @@ struct EpPeers {
   float* w_all[kMaxEpRanks];          // rank r's gathered router weights [T_all][K]
   int32_t* flags[kMaxEpRanks];        // rank r's barrier flags [world]
 };
+
+// flags[r] holds kMaxEpRanks barrier slots followed by rank r's sticky ABORT word: a
+// barrier that times out stores 1 into every rank's abort word; every later barrier fails
+// fast and the kernels that touch peer memory (router dispatch stores, combine loads/stores)
+// skip their peer accesses, so no rank proceeds on a half-synchronised step.
+constexpr int kEpAbortSlot = kMaxEpRanks;
+constexpr int kEpFlagWords = kMaxEpRanks + 1;
+__device__ __forceinline__ void st_release_sys(int32_t* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool ep_aborted(const EpPeers& ep) {
+  return ld_acquire_sys(ep.flags[ep.rank] + kEpAbortSlot) != 0;
+}
 
 // 1: the combine grid is launched with programmatic dependent launch and the FFN triggers
 // it when each CTA runs out of tickets, so combine CTAs start on the SMs the FFN's tail has

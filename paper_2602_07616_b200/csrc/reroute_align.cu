@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
   uint8_t* s_need = s_hflag + round_up(M, 4);
   uint8_t* s_cls = s_need + round_up(M, 4);
-  __shared__ int s_err_id, s_err_sim, s_err_route, s_nneed;
+  __shared__ int s_err_id, s_err_sim, s_err_route, s_err_domain, s_nneed;
 
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   const int s_eff = S < K ? S : K;  // S == K: identity re-routing, every routed expert is primary
   auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
 
-  if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; }
+  if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0; }
   for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
   if (align) {
     for (int i = tid; i < kAlignWarps * Et; i += nthr) s_bm[i] = 0u;
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         s_ids[k * T + t] = v;
         const bool ok = v >= 0 && v < M;
         bad |= !ok;
+        if (v == SERE_ID_NONFINITE) s_err_domain = 1;  // the router saw a non-finite token state
         if (reroute && ok && k < s_eff) s_hflag[v] = 1;  // primary set H (rerouting.py:147; Alg. 2 l.467-471)
       }
     }
@@ -136,7 +137,8 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   SERE_PHASE(1);
   if (s_err_id || s_err_sim) {
     if (tid == 0) {
-      const int code = s_err_id ? (reroute ? SERE_ERR_DIMENSION : SERE_ERR_ROUTING) : SERE_ERR_INPUT;
+      const int code = s_err_domain ? SERE_ERR_DOMAIN
+                                    : s_err_id ? (reroute ? SERE_ERR_DIMENSION : SERE_ERR_ROUTING) : SERE_ERR_INPUT;
       if (p.status_dev) *p.status_dev = code;
       if (p.plan) p.plan[P_STATUS] = code;
     }
@@ -492,13 +494,8 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
   const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, p.r_max);
-  static size_t configured = 0;
-  if (smem > 32 * 1024 && smem > configured) {  // dynamic + ~4 KB static may cross the 48 KB default
-    cudaError_t e = cudaFuncSetAttribute(reroute_align_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
+  if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
 }
 

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "../../include/sere_b200.h"
 #include "params.cuh"
 #include "ptx.cuh"
 #include "rowops.cuh"
@@ -50,10 +51,14 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
     for (int j = 0; j < kTok; ++j) s_part[(ks * kTok + j) * M + e] = acc[j];
   }
   __syncthreads();
+  __shared__ int s_bad[kTok];
+  if (threadIdx.x < kTok) s_bad[threadIdx.x] = 0;
+  __syncthreads();
   for (int i = threadIdx.x; i < kTok * M; i += blockDim.x) {
     float s = 0.f;
     for (int q = 0; q < KS; ++q) s += s_part[q * kTok * M + i];
     if (bias) s += bias[i % M];
+    if (!isfinite(s)) s_bad[i / M] = 1;  // non-finite token state -> SERE_ID_NONFINITE (DomainError)
     s_logit[i] = s;
   }
   __syncthreads();
@@ -80,9 +85,9 @@ __global__ void __launch_bounds__(1024) route_topk_kernel(const __nv_bfloat16* _
       }
       if (r == 0) top = bv;
       sel_val[r] = bv;
-      if (lane == 0) ids[static_cast<size_t>(t) * K + r] = bi;
+      if (lane == 0) ids[static_cast<size_t>(t) * K + r] = s_bad[warp] ? SERE_ID_NONFINITE : bi;
       __syncwarp();
-      if (lane == (bi & 31)) lg[bi] = -CUDART_INF_F;  // remove the pick (ties resolved on index above)
+      if (bi >= 0 && lane == (bi & 31)) lg[bi] = -CUDART_INF_F;  // remove the pick (ties resolved on index above)
       __syncwarp();
     }
     if (lane == 0) {
@@ -176,6 +181,8 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
   const int my_t0 = static_cast<int>(split) * tpc;
   const int my_rows = max(0, min(tpc, nt_valid - my_t0));
   float* gath = reinterpret_cast<float*>(rsm);  // [S][tpc][M] (own slot unused)
+  __shared__ int s_nonfinite[kRcTok];
+  for (int r = tid; r < kRcTok; r += blockDim.x) s_nonfinite[r] = 0;
   fence_proxy_async_smem();  // generic smem accesses above before the async-proxy copies below
   if (tid == 0 && my_rows > 0 && S > 1) mbar_arrive_expect_tx(&s_gather, static_cast<uint32_t>(my_rows * M * 4 * (S - 1)));
   cluster_sync_all();  // partials written, barriers armed, staging buffers no longer read
@@ -203,8 +210,15 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
       for (int q = 0; q < kRcMaxSplit; ++q)
         if (q < S) acc_l += pv[q];  // split order
       if (bias) acc_l += b;
-      lgt[i] = acc_l;
       if (logits_out) logits_out[static_cast<size_t>(t0 + my_t0) * M + i] = acc_l;
+      // a non-finite logit (non-finite token state: the reference raises DomainError,
+      // moe.py:274-275) flags its token; NaN is ranked as -inf so the top-K below stays a
+      // well-defined permutation
+      if (!isfinite(acc_l)) {
+        s_nonfinite[i / M] = 1;
+        if (isnan(acc_l)) acc_l = -INFINITY;
+      }
+      lgt[i] = acc_l;
     }
     __syncthreads();
     RC_PROBE(7);
@@ -234,12 +248,13 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
       for (int k = 0; k < K; ++k) den += __expf(sel_v[r * K + k] - top);
       if (lane < K) {
         const size_t o = static_cast<size_t>(t0 + my_t0 + r) * K + lane;
-        const int id = sel_i[r * K + lane];
+        const bool bad = s_nonfinite[r] != 0;
+        const int id = bad ? SERE_ID_NONFINITE : sel_i[r * K + lane];  // -> DomainError downstream
         const float wv = __expf(sel_v[r * K + lane] - top) / den;
         if (ep.world == 0) {
           ids[o] = id;
           weights[o] = wv;
-        } else {  // expert parallel: this rank's rows of every rank's gathered table (NVLink stores)
+        } else if (!ep_aborted(ep)) {  // expert parallel: this rank's rows of every rank's gathered table (NVLink stores)
           const size_t og = static_cast<size_t>(ep.t0) * K + o;
           for (int p = 0; p < ep.world; ++p) {
             ep.ids_all[p][og] = id;
@@ -500,13 +515,8 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
   if (T <= 0) return cudaSuccess;
   if (route_tc_path(M, K, d_h)) {
     const RouteTcGeom g = route_tc_geom(d_h, M);
-    static size_t configured_tc = 0;
-    if (g.smem > 48 * 1024 && g.smem > configured_tc) {
-      cudaError_t e = cudaFuncSetAttribute(route_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(g.smem));
-      if (e != cudaSuccess) return e;
-      configured_tc = g.smem;
-    }
+    static SmemAttrCache attr_tc;
+    if (cudaError_t e = ensure_smem_attr(route_tc_kernel, g.smem, attr_tc); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((T + kRtTok - 1) / kRtTok, g.S, 1);
     cfg.blockDim = dim3(kRcThreads, 1, 1);
@@ -526,13 +536,8 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
                               logits_out, g_route_dbg, ep ? *ep : none);
   }
   const RouteGeom g = route_geom(d_h, M);
-  static size_t configured = 0;
-  if (g.smem > 48 * 1024 && g.smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(route_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(g.smem));
-    if (e != cudaSuccess) return e;
-    configured = g.smem;
-  }
+  static SmemAttrCache smem_attr;
+  if (cudaError_t e = ensure_smem_attr(route_cluster_kernel, g.smem, smem_attr); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((T + kRcTok - 1) / kRcTok, g.S, 1);
   cfg.blockDim = dim3(kRcThreads, 1, 1);
@@ -563,13 +568,8 @@ cudaError_t launch_route_topk(const __nv_bfloat16* x, const __nv_bfloat16* w_rou
   if (threads > 1024) threads = 1024;
   const size_t smem = static_cast<size_t>(KS) * kTok * M * 4 + static_cast<size_t>(kTok) * M * 4 +
                       static_cast<size_t>(kTok) * d_h * 2;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(route_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  static SmemAttrCache smem_attr;
+  if (cudaError_t e = ensure_smem_attr(route_topk_kernel, smem, smem_attr); e != cudaSuccess) return e;
   const int blocks = (T + kTok - 1) / kTok;
   route_topk_kernel<<<blocks, threads, smem, stream>>>(x, w_router, bias, T, d_h, M, K, KS, ids, weights,
                                                         logits_out);

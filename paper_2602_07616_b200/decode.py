@@ -170,7 +170,11 @@ class DecodeStep(StageEvents):
         self.graph = None
         self.stage_events = None
         self._trace_hook = None  # debug_ffn: called with the layer index before each layer launch
-        _moe.workspace(T, model.K, model.M, model.n_shared, model.d_h, model.d_m, dev)
+        # this step's own workspaces: its CUDA graph bakes in their addresses, so they live
+        # (and are used) exactly as long as the step
+        self.ws = _moe.new_workspace(T, model.K, len(model.expert_ids), len(model.shared_ids), model.d_h,
+                                     model.d_m, dev)
+        self.route_ws = _moe.route_workspace(T, model.d_h, model.M, dev)
 
     # ---------------------------------------------------------------- launches
     def _norm(self, y) -> None:
@@ -190,16 +194,17 @@ class DecodeStep(StageEvents):
                     self.h.copy_(self.x)
                 else:
                     self.h.copy_(self.outs[l - 1].y)
-            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
+            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w),
+                                   ws=self.route_ws)
             if self._trace_hook is not None:
                 self._trace_hook(l)
             self._events_on(l)
             if plain:
                 _moe.moe_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
-                                        out=self.outs[l])
+                                        out=self.outs[l], ws=self.ws)
             else:  # x += MoE(h); h = RMSNorm(x) fused into the combine pass
                 _moe.moe_block_forward_device(layer.bank, layer.sim, self.S, self.rho, self.h, self.ids, self.w,
-                                              self.x, self.h, self.eps, out=self.outs[l])
+                                              self.x, self.h, self.eps, out=self.outs[l], ws=self.ws)
             self._events_off()
         if plain:
             self.x.copy_(self.outs[-1].y)
@@ -240,6 +245,11 @@ class DecodeStep(StageEvents):
 
     def set_input(self, x) -> None:
         self.x_in.copy_(x)
+
+    @property
+    def workspace(self) -> tuple[int, int]:
+        """(device pointer, bytes) of this step's layer workspace (kernel-only FFN replay)."""
+        return self.ws.data_ptr(), self.ws.numel()
 
     def run_host(self, x_host, out_host) -> None:
         """Public end-to-end call: host (pinned) input -> step -> host output, stream-ordered."""

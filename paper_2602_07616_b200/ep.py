@@ -165,7 +165,13 @@ class EPDecodeStep(StageEvents):
                                               rr.status, rr))
         self.graph = None
         self.graphed = False
-        _moe.workspace(T, model.K, len(model.expert_ids), len(model.shared_ids), model.d_h, model.d_m, dev)
+        self.ws = _moe.new_workspace(T, model.K, len(model.expert_ids), len(model.shared_ids), model.d_h,
+                                     model.d_m, dev)
+        self.route_ws = _moe.route_workspace(self.T_local, model.d_h, model.M, dev)
+
+    @property
+    def workspace(self) -> tuple[int, int]:
+        return self.ws.data_ptr(), self.ws.numel()
 
     def _norm(self, y) -> None:
         _lib.call("sere_residual_rmsnorm", self.x.data_ptr(), y.data_ptr() if y is not None else None,
@@ -176,11 +182,12 @@ class EPDecodeStep(StageEvents):
         self.x.copy_(self.x_in)
         self._norm(None)
         for l, layer in enumerate(m.layers):
-            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w))
+            _moe.route_topk_device(layer.w_router_t, self.h, m.K, bias=layer.bias, out=(self.ids, self.w),
+                                   ws=self.route_ws)
             h_all, ids_all, w_all = self.xch.gather(self.h, self.ids, self.w)
             self._events_on(l)
             _moe.moe_forward_ep_device(layer.bank, m.M, self.lo, layer.sim, self.S, self.rho, h_all, ids_all,
-                                       w_all, out=self.outs[l])
+                                       w_all, out=self.outs[l], ws=self.ws)
             self._events_off()
             y_local = self.xch.reduce_scatter(self.outs[l].y)
             self._norm(y_local)

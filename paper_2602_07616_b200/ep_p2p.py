@@ -73,7 +73,7 @@ class PeerRegion:
         self.off_w = off
         off = _align(off + T_all * K * 4, 1024)
         self.off_flags = off
-        off = _align(off + 4 * _lib.MAX_EP_RANKS, 1024)
+        off = _align(off + 4 * (_lib.MAX_EP_RANKS + 1), 1024)  # barrier slots + the sticky abort word
         self.off_ws = off
         self.ws_bytes = ws_bytes
         self.nbytes = off + ws_bytes + 2048
@@ -102,7 +102,7 @@ class PeerRegion:
         self.h_all = _view(base + self.off_h, (T, d_h), "<i2", dev).view(torch.bfloat16)
         self.ids_all = _view(base + self.off_ids, (T, K), "<i4", dev)
         self.w_all = _view(base + self.off_w, (T, K), "<f4", dev)
-        self.flags = _view(base + self.off_flags, (_lib.MAX_EP_RANKS,), "<i4", dev)
+        self.flags = _view(base + self.off_flags, (_lib.MAX_EP_RANKS + 1,), "<i4", dev)
         self.ws_ptr = _align(base + self.off_ws, 1024)  # the library aligns its workspace base to 1 KB too
 
     def ipc_handle(self) -> bytes:

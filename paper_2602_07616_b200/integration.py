@@ -22,6 +22,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Any
 
+import numpy as np
+
 from . import moe as _moe
 from . import rerouting as _rr
 
@@ -48,18 +50,40 @@ class Installed:
 
 def install(rerouting_module: Any, moe_module: Any | None = None) -> Installed:
     """Point `rerouting_module.apply_sere` (rerouting.py:130) and, if given,
-    `moe_module.layer_forward` (moe.py:280) at the GPU implementations."""
+    `moe_module.layer_forward` (moe.py:280) at the GPU implementations.
+
+    The device path has size limits the reference does not (T*K <= 16384 cells, M <= 256
+    routed and <= 31 shared experts, `moe.device_supports`); a call beyond them runs the
+    saved reference function instead, so every caller keeps working. The installed
+    wrappers resolve this package's implementations at call time."""
     result_cls = getattr(rerouting_module, "RerouteResult", None)
+    ref_apply_sere = rerouting_module.apply_sere
+    saved = {(rerouting_module, "apply_sere"): ref_apply_sere}
 
     def apply_sere(assignment, sim, config):
+        shape = np.shape(getattr(assignment, "indices", assignment))
+        m = np.shape(getattr(sim, "values", sim))
+        if len(shape) != 2 or len(m) != 2 or not _rr.device_supports(shape[0], shape[1], m[0]):
+            return ref_apply_sere(assignment, sim, config)  # the reference's limits / its own errors
         return _adapt_result(_rr.apply_sere(assignment, sim, config), result_cls)
 
     apply_sere.__doc__ = _rr.apply_sere.__doc__
-    saved = {(rerouting_module, "apply_sere"): rerouting_module.apply_sere}
     rerouting_module.apply_sere = apply_sere
     if moe_module is not None:
-        saved[(moe_module, "layer_forward")] = moe_module.layer_forward
-        moe_module.layer_forward = _moe.layer_forward
+        ref_layer_forward = moe_module.layer_forward
+        saved[(moe_module, "layer_forward")] = ref_layer_forward
+
+        def layer_forward(layer, x, assignment, activation="silu"):
+            idx = getattr(assignment, "indices", None)
+            shape = getattr(idx, "shape", ())
+            ok = len(shape) == 2 and _moe.device_supports(int(shape[0]), int(shape[1]), len(layer.experts),
+                                                          len(getattr(layer, "shared_experts", ())))
+            if not ok:
+                return ref_layer_forward(layer, x, assignment, activation)
+            return _moe.layer_forward(layer, x, assignment, activation)
+
+        layer_forward.__doc__ = _moe.layer_forward.__doc__
+        moe_module.layer_forward = layer_forward
     return Installed(rerouting_module, moe_module, saved)
 
 

@@ -106,28 +106,49 @@ def load_model(directory, device=None, chunk: int = 8) -> GpuModel:
     return GpuModel(layers, d_h, act, meta.get("seed"))
 
 
-def save_model(model: GpuModel, directory) -> None:
-    """moe.py:440-473 from GPU banks (bf16 values written as float32)."""
+def model_meta(seed, n_layers: int, n_experts: int, top_k: int, d_h: int, d_m: int, n_shared: int,
+               activation: str) -> dict:
+    """model.json of moe.py:445-454 (same keys, same order)."""
+    return {"seed": seed, "n_layers": n_layers, "n_experts": n_experts, "top_k": top_k, "d_h": d_h, "d_m": d_m,
+            "n_shared": n_shared, "activation": activation}
+
+
+def write_model_dir(directory, meta: dict, layers) -> None:
+    """The byte layout of the reference's save_model (moe.py:440-473): model.json, then per
+    layer the routed experts' gate/up/down, the shared experts', and the router, each a
+    little-endian float32 row-major file. `layers` yields (w_gate [E,d_h,d_m], w_up,
+    w_down [E,d_m,d_h], w_router [d_h,M]) host arrays with the routed experts first."""
     directory = Path(directory)
     directory.mkdir(parents=True, exist_ok=True)
+    (directory / MODEL_META_NAME).write_text(json.dumps(meta, indent=2) + "\n")
+    n_routed = int(meta["n_experts"])
+    for l, (wg, wu, wd, w_router) in enumerate(layers):
+        for j in range(len(wg)):
+            name = f"expert{j}" if j < n_routed else f"shared{j - n_routed}"
+            _write_f32(directory / f"layer{l}.{name}.gate.f32", wg[j])
+            _write_f32(directory / f"layer{l}.{name}.up.f32", wu[j])
+            _write_f32(directory / f"layer{l}.{name}.down.f32", wd[j])
+        _write_f32(directory / f"layer{l}.router.f32", w_router)
+
+
+def save_model(model: GpuModel, directory) -> None:
+    """moe.py:440-473 from GPU banks (bf16 values written as float32), one layer's
+    tensors on the host at a time."""
     first = model.layers[0]
-    meta = {"seed": model.seed, "n_layers": model.n_layers, "n_experts": first.bank.M,
-            "top_k": first.router.top_k, "d_h": model.d_h, "d_m": first.bank.d_m,
-            "n_shared": first.bank.n_shared, "activation": model.activation}
+    meta = model_meta(model.seed, model.n_layers, first.bank.M, first.router.top_k, model.d_h, first.bank.d_m,
+                      first.bank.n_shared, model.activation)
     for layer in model.layers:
         b = layer.bank
         if (b.M, b.n_shared, b.d_m, layer.router.top_k) != (meta["n_experts"], meta["n_shared"], meta["d_m"],
                                                           meta["top_k"]):
             raise ConfigError("only homogeneous layer stacks can be serialized")
-    (directory / MODEL_META_NAME).write_text(json.dumps(meta, indent=2) + "\n")
-    for l, layer in enumerate(model.layers):
-        wg, wu, wd = (t.float().cpu().numpy() for t in layer.bank.unpack())
-        for j in range(layer.bank.n_total):
-            name = f"expert{j}" if j < layer.bank.M else f"shared{j - layer.bank.M}"
-            _write_f32(directory / f"layer{l}.{name}.gate.f32", wg[j])
-            _write_f32(directory / f"layer{l}.{name}.up.f32", wu[j])
-            _write_f32(directory / f"layer{l}.{name}.down.f32", wd[j])
-        _write_f32(directory / f"layer{l}.router.f32", layer.router.w_router.float().cpu().numpy())
+
+    def host_layers():
+        for layer in model.layers:
+            wg, wu, wd = (t.float().cpu().numpy() for t in layer.bank.unpack())
+            yield wg, wu, wd, layer.router.w_router.float().cpu().numpy()
+
+    write_model_dir(directory, meta, host_layers())
 
 
 # ---------------------------------------------------------------------------
@@ -190,5 +211,5 @@ def save_similarity(values, directory, layer_index: int = 0, metric: str = "frob
     return path
 
 
-__all__ = ["GpuModel", "GpuLayer", "GpuRouter", "load_model", "save_model", "load_similarity",
+__all__ = ["GpuModel", "GpuLayer", "GpuRouter", "load_model", "save_model", "write_model_dir", "model_meta", "load_similarity",
            "load_similarity_set", "save_similarity", "validate_similarity", "MODEL_META_NAME"]

@@ -163,15 +163,30 @@ class ExpertBank:
 # ---------------------------------------------------------------------------
 
 _WS: dict = {}
+_WS_RETIRED: list = []  # grown-out buffers are kept alive: a captured graph may still point at them
+
+
+def workspace_bytes(T: int, K: int, M: int, n_shared: int, d_h: int, d_m: int) -> int:
+    return int(_lib.load().sere_layer_workspace_bytes(T, K, M, n_shared, d_h, d_m))
+
+
+def new_workspace(T: int, K: int, M: int, n_shared: int, d_h: int, d_m: int, device) -> Any:
+    """A caller-owned layer workspace (plan, permutation, x/h packs, expert outputs). Anything
+    that captures a CUDA graph or runs on its own stream owns one (DecodeStep does)."""
+    torch = _torch()
+    return torch.empty(max(workspace_bytes(T, K, M, n_shared, d_h, d_m), 1), dtype=torch.uint8, device=device)
 
 
 def workspace(T: int, K: int, M: int, n_shared: int, d_h: int, d_m: int, device) -> Any:
-    torch = _torch()
-    nbytes = _lib.load().sere_layer_workspace_bytes(T, K, M, n_shared, d_h, d_m)
+    """Shared per-device workspace for ad-hoc calls on the current stream (grown on demand;
+    a replaced buffer is retired, never freed)."""
+    nbytes = workspace_bytes(T, K, M, n_shared, d_h, d_m)
     key = (str(device),)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        if buf is not None:
+            _WS_RETIRED.append(buf)
+        buf = new_workspace(T, K, M, n_shared, d_h, d_m, device)
         _WS[key] = buf
     return buf
 
@@ -200,7 +215,7 @@ def _check_layer_inputs(bank: ExpertBank, x, ids, weights):
 
 
 def layer_forward_device(bank: ExpertBank, x, ids, weights, activation: str = "silu", y=None, y_bf16=None,
-                         status=None, stream=None, want_bf16: bool = False) -> LayerOutput:
+                         status=None, stream=None, want_bf16: bool = False, ws=None) -> LayerOutput:
     """moe.py:280-310 on CUDA tensors: x bf16 [T,d_h], ids int32 [T,K], weights f32 [T,K]."""
     torch = _torch()
     x, ids, weights = _check_layer_inputs(bank, x, ids, weights)
@@ -210,7 +225,7 @@ def layer_forward_device(bank: ExpertBank, x, ids, weights, activation: str = "s
     if want_bf16 and y_bf16 is None:
         y_bf16 = torch.empty((T, bank.d_h), dtype=torch.bfloat16, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev) if status is None else status
-    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev) if ws is None else ws
     _lib.call("sere_layer_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
               activation_code(activation), x.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, y.data_ptr(),
               y_bf16.data_ptr() if y_bf16 is not None else None, ws.data_ptr(), ws.numel(), status.data_ptr(),
@@ -220,7 +235,7 @@ def layer_forward_device(bank: ExpertBank, x, ids, weights, activation: str = "s
 
 def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: float, x, ids, weights,
                        activation: str = "silu", stream=None, want_bf16: bool = False,
-                       out: LayerOutput | None = None) -> LayerOutput:
+                       out: LayerOutput | None = None, ws=None) -> LayerOutput:
     """Fused SERE layer (moe.py:367-375): re-route `ids` against `sim`, then run the
     layer on the rewritten ids with the ORIGINAL weights (moe.py:369). S == K gives
     plain top-k on the same kernels."""
@@ -248,7 +263,7 @@ def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: floa
                           rr.status, rr)
     rr = out.reroute
     flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
-    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev) if ws is None else ws
     _lib.call("sere_moe_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
               activation_code(activation), dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags,
               x.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, rr.new_indices.data_ptr(),
@@ -262,7 +277,7 @@ def moe_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: floa
 
 def moe_block_forward_device(bank: ExpertBank, sim, retain_count: int, threshold: float, h, ids, weights,
                              x_residual, h_next, eps: float = 1e-6, activation: str = "silu", stream=None,
-                             out: LayerOutput | None = None, want_y: bool = False) -> LayerOutput:
+                             out: LayerOutput | None = None, want_y: bool = False, ws=None) -> LayerOutput:
     """Decode block (`sere_moe_block_forward`): x_residual += SERE-MoE(h) and
     h_next = bf16(RMSNorm(x_residual)) in the combine pass. h_next may alias h."""
     import ctypes
@@ -285,7 +300,7 @@ def moe_block_forward_device(bank: ExpertBank, sim, retain_count: int, threshold
         out = LayerOutput(y, None, rr.status, rr)
     rr = out.reroute
     flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
-    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev) if ws is None else ws
     _lib.call("sere_moe_block_forward", bank.data.data_ptr(), bank.M, bank.n_shared, bank.d_h, bank.d_m,
               activation_code(activation), dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags,
               h.data_ptr(), ids.data_ptr(), weights.data_ptr(), T, K, rr.new_indices.data_ptr(),
@@ -299,7 +314,7 @@ def moe_block_forward_device(bank: ExpertBank, sim, retain_count: int, threshold
 
 def moe_forward_ep_device(bank: ExpertBank, n_experts: int, expert_lo: int, sim, retain_count: int,
                           threshold: float, x, ids, weights, activation: str = "silu", stream=None,
-                          out: LayerOutput | None = None) -> LayerOutput:
+                          out: LayerOutput | None = None, ws=None) -> LayerOutput:
     """Expert-parallel shard of `moe_forward_device` (`sere_moe_forward_ep`): re-route the
     full gathered [T,K] table against `sim` (global ids, M = n_experts), then evaluate only
     this bank's experts (global [expert_lo, expert_lo + bank.M) + its shared experts).
@@ -330,7 +345,7 @@ def moe_forward_ep_device(bank: ExpertBank, n_experts: int, expert_lo: int, sim,
         out = LayerOutput(torch.empty((T, bank.d_h), dtype=torch.float32, device=dev), None, rr.status, rr)
     rr = out.reroute
     flags = 0 if dsim.validated else _rr.FLAG_CHECK_SIM
-    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev)
+    ws = workspace(T, K, bank.M, bank.n_shared, bank.d_h, bank.d_m, dev) if ws is None else ws
     _lib.call("sere_moe_forward_ep", bank.data.data_ptr(), int(n_experts), int(expert_lo),
               int(expert_lo) + bank.M, bank.n_shared, bank.d_h, bank.d_m, activation_code(activation),
               dsim.values.data_ptr(), cfg.retain_count, cfg.threshold, flags, x.data_ptr(), ids.data_ptr(),
@@ -350,7 +365,14 @@ def router_weight_t(w_router):
     return w_router.to(torch.bfloat16).t().contiguous()
 
 
-def route_topk_device(w_router_t, x, top_k: int, stream=None, logits: bool = False, bias=None, out=None):
+def route_workspace(T: int, d_h: int, M: int, device) -> Any:
+    """A caller-owned router workspace (zero-initialised: its tickets start at zero)."""
+    torch = _torch()
+    return torch.zeros(max(int(_lib.load().sere_route_workspace_bytes(T, d_h, M)), 1), dtype=torch.uint8,
+                       device=device)
+
+
+def route_topk_device(w_router_t, x, top_k: int, stream=None, logits: bool = False, bias=None, out=None, ws=None):
     """moe.py:268-277 on CUDA: w_router_t bf16 [M, d_h] (see `router_weight_t`), x bf16 [T,d_h]
     -> (ids int32 [T,K], weights f32 [T,K][, logits f32 [T,M]]).
     `bias` (f32 [M], optional) is the benchmark's popularity-skew knob added to the logits."""
@@ -370,12 +392,15 @@ def route_topk_device(w_router_t, x, top_k: int, stream=None, logits: bool = Fal
         wts = torch.empty((T, top_k), dtype=torch.float32, device=x.device)
     lg = torch.empty((T, M), dtype=torch.float32, device=x.device) if logits else None
     b = bias.to(torch.float32).contiguous() if bias is not None else None
-    nbytes = _lib.load().sere_route_workspace_bytes(T, d_h, M)
-    key = str(x.device)
-    ws = _ROUTE_WS.get(key)
-    if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=x.device)  # tickets start at zero
-        _ROUTE_WS[key] = ws
+    if ws is None:
+        nbytes = _lib.load().sere_route_workspace_bytes(T, d_h, M)
+        key = str(x.device)
+        ws = _ROUTE_WS.get(key)
+        if ws is None or ws.numel() < nbytes:
+            if ws is not None:
+                _WS_RETIRED.append(ws)
+            ws = route_workspace(T, d_h, M, x.device)
+            _ROUTE_WS[key] = ws
     _lib.call("sere_route_topk", x.data_ptr(), w.data_ptr(), b.data_ptr() if b is not None else None,
               T, d_h, M, int(top_k), ids.data_ptr(), wts.data_ptr(), lg.data_ptr() if lg is not None else None,
               ws.data_ptr(), ws.numel(), _stream_ptr(stream))
@@ -386,23 +411,74 @@ def route_topk_device(w_router_t, x, top_k: int, stream=None, logits: bool = Fal
 # reference-shaped drop-ins (host arrays in/out)
 # ---------------------------------------------------------------------------
 
-_BANKS: dict[int, tuple[Any, ExpertBank]] = {}
+MAX_CELLS = 16384   # T*K of one layer call (the align kernel's u16 counters and smem ids; capi.cu kMaxCells)
+MAX_EXPERTS = 256   # routed experts per layer (capi.cu kMaxExperts)
+MAX_SHARED = 31     # shared experts per layer (capi.cu kMaxShared)
 
 
-def bank_for(layer: Any) -> ExpertBank:
-    """ExpertBank of a reference MoELayer, converted once and cached by identity."""
+def device_supports(n_tokens: int, top_k: int, n_experts: int, n_shared: int = 0) -> bool:
+    """Whether one layer call of this shape fits the device path's limits (the reference
+    itself has none; `integration.install` falls back to the reference function beyond them)."""
+    return (n_tokens * top_k <= MAX_CELLS and 1 <= n_experts <= MAX_EXPERTS and 0 <= n_shared <= MAX_SHARED
+            and 1 <= top_k <= n_experts)
+
+
+def _fingerprint(a: Any) -> tuple:
+    """Content key of one weight array: shape, dtype, wrapping uint64 sum and xor of its
+    words. Any single changed element changes the sum; read once at memory bandwidth,
+    which is the same traffic the reference's own expert_forward spends on the array."""
+    a = np.ascontiguousarray(np.asarray(a))
+    b = a.reshape(-1).view(np.uint8)
+    n8 = b.size // 8 * 8
+    w = b[:n8].view(np.uint64)
+    tail = bytes(b[n8:])
+    return (a.shape, a.dtype.str, int(w.sum(dtype=np.uint64)), int(np.bitwise_xor.reduce(w)) if w.size else 0, tail)
+
+
+def _expert_fingerprint(e: Any) -> tuple:
+    return (_fingerprint(e.w_gate), _fingerprint(e.w_up), _fingerprint(e.w_down))
+
+
+_BANKS: dict[int, tuple[Any, ExpertBank, list]] = {}
+
+
+def bank_for(layer: Any, experts_used=None) -> ExpertBank:
+    """ExpertBank of a reference MoELayer, packed once and kept in sync with the layer's
+    CONTENT: every call fingerprints the experts it is about to use (`experts_used` = bank
+    slots, default all) and re-packs any whose weights changed in place since they were
+    packed. The reference reads the current arrays on every call (moe.py:243-245), so an
+    edited weight must never be served from a stale device copy."""
     if isinstance(layer, ExpertBank):
         return layer
     if isinstance(getattr(layer, "bank", None), ExpertBank):  # io.GpuLayer
         return layer.bank
+    experts = list(layer.experts) + list(getattr(layer, "shared_experts", ()))
     hit = _BANKS.get(id(layer))
-    if hit is not None and hit[0] is layer:
-        return hit[1]
-    bank = ExpertBank.from_reference_layer(layer)
-    if len(_BANKS) > 256:
-        _BANKS.clear()
-    _BANKS[id(layer)] = (layer, bank)
+    if hit is None or hit[0] is not layer:
+        bank = ExpertBank.from_reference_layer(layer)
+        if len(_BANKS) > 64:
+            _BANKS.clear()
+        _BANKS[id(layer)] = (layer, bank, [_expert_fingerprint(e) for e in experts])
+        return bank
+    _, bank, fps = hit
+    torch = _torch()
+    for j in (range(len(experts)) if experts_used is None else experts_used):
+        fp = _expert_fingerprint(experts[j])
+        if fp != fps[j]:
+            e = experts[j]
+            t = [torch.from_numpy(np.asarray(getattr(e, n), dtype=np.float32)[None]).to(bank.device, torch.bfloat16)
+                 for n in ("w_gate", "w_up", "w_down")]
+            bank.pack(*t, first=j)
+            fps[j] = fp
     return bank
+
+
+def invalidate(layer: Any | None = None) -> None:
+    """Forget the packed copy of `layer` (or of every layer)."""
+    if layer is None:
+        _BANKS.clear()
+    else:
+        _BANKS.pop(id(layer), None)
 
 
 def layer_forward(layer: Any, x: Any, assignment: Any, activation: str = "silu") -> np.ndarray:
@@ -411,18 +487,21 @@ def layer_forward(layer: Any, x: Any, assignment: Any, activation: str = "silu")
     device result widened)."""
     torch = _torch()
     activation_code(activation)
-    bank = bank_for(layer)
+    idx = np.asarray(assignment.indices)
+    n_routed = len(layer.experts) if not isinstance(layer, ExpertBank) and hasattr(layer, "experts") else None
+    used = None
+    if n_routed is not None and idx.size and idx.min() >= 0 and idx.max() < n_routed:
+        n_sh = len(getattr(layer, "shared_experts", ()))
+        used = sorted(set(np.unique(idx).tolist()) | set(range(n_routed, n_routed + n_sh)))
+    bank = bank_for(layer, used)
     xa = np.asarray(x, dtype=np.float64)
     if xa.ndim != 2:
         raise DimensionError(f"x must be 2-D, got shape {xa.shape}")
-    idx = np.asarray(assignment.indices)
     w = np.asarray(assignment.weights, dtype=np.float64)
     if idx.shape[0] != xa.shape[0]:
         raise DimensionError(f"assignment covers {idx.shape[0]} tokens, batch has {xa.shape[0]}")
     if xa.shape[1] != bank.d_h:
         raise DimensionError(f"input width {xa.shape[1]} does not match expert d_h {bank.d_h}")
-    if not np.all(np.isfinite(xa)):
-        raise DomainError("expert input contains non-finite values")
     if idx.size and (idx.min() < 0 or idx.max() >= bank.M):
         raise RoutingError(f"assignment refers to experts outside [0, {bank.M})")
     dev = bank.device
@@ -470,8 +549,15 @@ def route_topk(router: Any, x: Any) -> Assignment:
     """moe.py:268-277 on the GPU for a reference RouterWeights (bf16 weights, fp32 logits)."""
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device())
+    xa = np.asarray(x, dtype=np.float64)
+    if xa.ndim != 2:
+        raise DimensionError(f"x must be 2-D, got shape {xa.shape}")
+    if xa.shape[1] != np.shape(router.w_router)[0]:
+        raise DimensionError(f"input width {xa.shape[1]} does not match router d_h {np.shape(router.w_router)[0]}")
+    if not np.all(np.isfinite(xa)):  # moe.py:274-275
+        raise DomainError("router input contains non-finite values")
     w = torch.as_tensor(np.asarray(router.w_router, dtype=np.float32)).to(dev)
-    xt = torch.as_tensor(np.asarray(x, dtype=np.float32)).to(dev)
+    xt = torch.as_tensor(xa.astype(np.float32)).to(dev)
     ids, wts = route_topk_device(router_weight_t(w), xt, int(router.top_k))
     return Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
 
@@ -509,7 +595,7 @@ def model_forward(model: Any, batch: Any, config: Any = None, sims: Sequence | N
             ids, wts = route_topk_device(router_weight_t(wr.to(dev)), x, int(layer.router.top_k))
             original = Assignment(ids.cpu().numpy().astype(np.int64), wts.double().cpu().numpy())
         if apply_rewrite:
-            dsim = _rr._cached_sim(sims[l], dev)
+            dsim = _rr.DeviceSimilarity(sims[l], dev)  # current values, validated on this call (rerouting.py:140)
             out = moe_forward_device(bank, dsim, config.retain_count, config.threshold, x, ids, wts,
                                      model.activation)
             out.check()

@@ -178,23 +178,13 @@ def reroute(ids, sim: Any, retain_count: int, threshold: float, stream=None, out
     return out
 
 
-_SIM_CACHE: dict[int, tuple[Any, DeviceSimilarity]] = {}
+MAX_CELLS = 16384  # T*K per call (capi.cu kMaxCells)
+MAX_EXPERTS = 256  # capi.cu kMaxExperts
 
 
-def _cached_sim(sim: Any, device) -> DeviceSimilarity:
-    """Upload a reference SimilarityMatrix once (keyed by its values array)."""
-    if isinstance(sim, DeviceSimilarity):
-        return sim
-    vals = getattr(sim, "values", sim)
-    key = id(vals)
-    hit = _SIM_CACHE.get(key)
-    if hit is not None and hit[0] is vals:
-        return hit[1]
-    ds = DeviceSimilarity(vals, device)
-    if len(_SIM_CACHE) > 4096:
-        _SIM_CACHE.clear()
-    _SIM_CACHE[key] = (vals, ds)
-    return ds
+def device_supports(n_tokens: int, top_k: int, n_experts: int) -> bool:
+    """Whether `sere_reroute` takes this shape (`integration.install` falls back beyond it)."""
+    return n_tokens * top_k <= MAX_CELLS and 1 <= n_experts <= MAX_EXPERTS
 
 
 def apply_sere(assignment: Any, sim: Any, config: RerouteConfig) -> RerouteResult:
@@ -211,16 +201,18 @@ def apply_sere(assignment: Any, sim: Any, config: RerouteConfig) -> RerouteResul
     if int(config.retain_count) > k:  # order of _validate_inputs: config first
         raise ConfigError(f"retain_count must not exceed K (got S={config.retain_count}, K={k})")
     dev = torch.device("cuda", torch.cuda.current_device())
-    dsim = _cached_sim(sim, dev)
+    # stateless like the reference: the CURRENT values are uploaded (M*M*8 B, 128 KiB at
+    # M=128) and range-checked on every call (rerouting.py:140, _validate_inputs 108-116);
+    # only the device-level API (`reroute` with a DeviceSimilarity) keeps a resident copy
+    dsim = sim if isinstance(sim, DeviceSimilarity) else DeviceSimilarity(sim, dev)
     if idx.size and (idx.min() < np.iinfo(np.int32).min or idx.max() > np.iinfo(np.int32).max):
         raise DimensionError(f"similarity matrix of dimension {dsim.m} does not cover every routed index")
     ids = torch.as_tensor(idx.astype(np.int32)).to(dev)
-    was_validated = dsim.validated
-    res = reroute(ids, dsim, int(config.retain_count), float(config.threshold))
+    res = reroute(ids, dsim, int(config.retain_count), float(config.threshold), check_sim=True)
     try:
         return res.to_result()
     except InputError:
-        dsim.validated = was_validated
+        dsim.validated = False
         raise
 
 
@@ -277,6 +269,7 @@ def load_trace(path) -> dict:
 
 __all__ = [
     "PHASE_MODES", "RerouteConfig", "RerouteResult", "DeviceSimilarity", "DeviceReroute", "reroute",
+    "device_supports",
     "apply_sere", "select_primary", "final_active_set", "result_to_dict", "result_from_dict",
     "save_trace", "load_trace", "SereError",
 ]

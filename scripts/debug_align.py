@@ -1,9 +1,14 @@
 """Phase timing of the re-routing/align kernel (clock64 after each barrier phase).
 
-    python -m paper_2602_07616_b200.debug_align [--T 512 --M 128 --K 8]
+    python scripts/debug_align.py [--T 512 --M 128 --K 8]
 """
 
 from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import argparse
 
@@ -19,9 +24,9 @@ def main() -> None:
     import numpy as np
     import torch
 
-    from . import _lib, build
-    from .decode import uniform_sim
-    from .rerouting import DeviceSimilarity, reroute
+    from paper_2602_07616_b200 import _lib, build
+    from paper_2602_07616_b200.decode import uniform_sim
+    from paper_2602_07616_b200.rerouting import DeviceSimilarity, reroute
 
     build.build()
     T, M, K = a.T, a.M, a.K
@@ -40,7 +45,7 @@ def main() -> None:
     d = np.diff(c[:n])
     print("reroute-only phases (cycles):", d.tolist(), "total", int(c[n - 1] - c[0]))
 
-    from .moe import ExpertBank, moe_forward_device
+    from paper_2602_07616_b200.moe import ExpertBank, moe_forward_device
 
     bank = ExpertBank.random(M, 0, 256, 128, seed=0)  # small dims: only the align kernel matters here
     x = torch.randn(T, 256, device="cuda").to(torch.bfloat16)

@@ -1,6 +1,6 @@
 """Per-CTA timeline of the fused FFN kernel (sere_debug_set_ffn_trace) on C4-shaped layers.
 
-    python -m paper_2602_07616_b200.debug_ffn [--layers 4 --mode sere --out gpurun_out/ffn_trace.npz]
+    python scripts/debug_ffn.py [--layers 4 --mode sere --out gpurun_out/ffn_trace.npz]
 
 Prints, per traced layer: kernel span, the spread of CTA start/end times (tail),
 and the average per-CTA wait split (producer slot-wait = ring full, MMA operand
@@ -8,6 +8,11 @@ wait = bytes not landed, dependency wait, accumulator wait, epilogue wait).
 """
 
 from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import argparse
 
@@ -25,8 +30,8 @@ def main() -> None:
     import numpy as np
     import torch
 
-    from . import _lib, build
-    from .decode import DecodeModel, DecodeStep
+    from paper_2602_07616_b200 import _lib, build
+    from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
 
     build.build()
     lib = _lib.load()

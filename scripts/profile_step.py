@@ -1,15 +1,20 @@
 """Profiling driver: a short C4-shaped decode run bracketed by cudaProfilerStart/Stop.
 
     ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
-        --csv --log-file gpurun_out/launches.csv python -m paper_2602_07616_b200.profile_step
+        --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py
     ncu --profile-from-start off --set full --import-source on -k regex:moe_ffn -c 2 \
-        -o gpurun_out/prof python -m paper_2602_07616_b200.profile_step --layers 2
+        -o gpurun_out/prof python scripts/profile_step.py --layers 2
 
 Only the profiled steps are inside the profiler range (weight generation, packing and
 warm-up are not), launched eagerly so every kernel appears as its own launch.
 """
 
 from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import argparse
 
@@ -25,8 +30,8 @@ def main() -> None:
 
     import torch
 
-    from . import build
-    from .decode import DecodeModel, DecodeStep
+    from paper_2602_07616_b200 import build
+    from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
 
     build.build()
     model = DecodeModel(a.layers, 128, 8, 2048, 768, seed=0, beta=a.beta)

@@ -38,9 +38,24 @@ def test_normalize_to_unit_matches_reference(metric):
         np.testing.assert_array_equal(normalize_to_unit(raw, metric), want)
 
 
+def test_calibration_activation_names_match_reference():
+    """Every activation the reference accepts (moe.py:22: silu, relu, gelu-tanh) is accepted
+    by the calibration (it builds the dense expert slabs with the same activation)."""
+    from paper_2602_07616_b200 import calibrate
+    from paper_2602_07616_b200.errors import ConfigError
+    from paper_2602_07616_b200.moe import ACTIVATIONS
+
+    assert ACTIVATIONS == O.ACTIVATIONS == ("silu", "relu", "gelu-tanh")
+    for a in ACTIVATIONS:
+        calibrate._act(a)
+    with pytest.raises(ConfigError):
+        calibrate._act("gelu_tanh")
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("metric", ["frobenius", "cosine"])
-def test_gpu_calibration_vs_oracle(cuda_device, metric):
+@pytest.mark.parametrize("metric,activation", [("frobenius", "silu"), ("cosine", "silu"),
+                                               ("frobenius", "gelu-tanh"), ("cosine", "relu")])
+def test_gpu_calibration_vs_oracle(cuda_device, metric, activation):
     import torch
 
     from paper_2602_07616_b200 import calibrate, io
@@ -56,12 +71,17 @@ def test_gpu_calibration_vs_oracle(cuda_device, metric):
         bank = ExpertBank.from_reference_layer(l, device="cuda")
         wr = torch.as_tensor(l.w_router, dtype=torch.float32, device="cuda").to(torch.bfloat16)
         gpu_layers.append(io.GpuLayer(bank, io.GpuRouter(wr, l.top_k)))
-    model = io.GpuModel(gpu_layers, layers[0].w_router.shape[0], "silu")
-    want = [O.normalize_to_unit(r, metric) for r in O.estimate_similarity_raw(layers, batches, metric)]
-    got = calibrate.estimate_similarity(model, batches, metric)
+    model = io.GpuModel(gpu_layers, layers[0].w_router.shape[0], activation)
+    want = [O.normalize_to_unit(r, metric)
+            for r in O.estimate_similarity_raw(layers, batches, metric, activation)]
+    got = calibrate.estimate_similarity(model, batches, metric, activation)
+    # these are similarity VALUES in [0, 1] (not layer outputs): layer 0 sees identical inputs
+    # (bf16 GEMMs vs fp64 only); layer 1 sees the GPU's routed forward of layer 0, whose bf16
+    # rounding can move a near-tied token to another expert, hence the looser bound there
     for l, (g, w) in enumerate(zip(got, want)):
         err = float(np.abs(g - w).max())
-        assert err <= (5e-3 if l == 0 else 2e-2), (metric, l, err)
+        print(f"calibration {metric} {activation} layer {l}: max-abs {err:.3e}")
+        assert err <= (5e-3 if l == 0 else 2e-2), (metric, activation, l, err)
     # the partner each expert would be re-routed to is (near-)optimal under the oracle's matrix
     off = ~np.eye(want[0].shape[0], dtype=bool)
     g0 = np.where(off, got[0], -1.0)

@@ -85,6 +85,20 @@ def test_p2p_barrier_times_out_instead_of_hanging(cuda_device):
         torch.cuda.synchronize()
         with pytest.raises(SereError):
             st.check()
+        # the timeout is sticky and visible to every rank: both abort words are raised, and the
+        # peer's next barrier fails at once (it would otherwise wait out its own 5 s timeout)
+        assert [int(s.region.flags[_lib.MAX_EP_RANKS].item()) for s in steps] == [1, 1]
+        peer = steps[1]
+        peer.timeout_ns = int(5e9)
+        import time
+
+        t0 = time.perf_counter()
+        _lib.call("sere_ep_barrier", ctypes.byref(peer.peers), peer.epoch.data_ptr(), peer.bar_status.data_ptr(),
+                  ctypes.c_int64(peer.timeout_ns), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert time.perf_counter() - t0 < 1.0
+        with pytest.raises(SereError):
+            peer.check()
     finally:
         for st in steps:
             st.close()

@@ -1,8 +1,9 @@
 """MoE layer parity: count/align plan (integer-exact), pack/unpack, grouped tcgen05 FFN.
 
-Tolerance (stated, north star): against the fp64 oracle / fp32 torch reference on the
-SAME bf16-rounded weights and inputs, the fp32 layer output must satisfy
-max|y - y_ref| <= 1e-2 * max(1, max|y_ref|) ... and cosine >= 0.9999.
+Tolerance (stated, north star, ABSOLUTE): against the fp64 oracle / fp32 torch reference on
+the SAME bf16-rounded weights and inputs, the fp32 layer output must satisfy
+max|y - y_ref| <= 1e-2 and cosine >= 0.9999 (conftest.check_close; measured values are
+logged to $SERE_PARITY_LOG).
 (The kernel rounds the SwiGLU intermediate h to bf16, as any bf16 grouped GEMM does.)
 """
 
@@ -15,25 +16,12 @@ from oracle import sere_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ATOL = 1e-2
-COS = 0.9999
-
+from conftest import check_close as _check_close
 
 def _bf16_round(a):
     import torch
 
     return torch.as_tensor(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
-
-
-def _check_close(y, ref, tag=""):
-    y = np.asarray(y, dtype=np.float64)
-    ref = np.asarray(ref, dtype=np.float64)
-    err = np.abs(y - ref).max() if y.size else 0.0
-    scale = max(1.0, float(np.abs(ref).max()) if ref.size else 1.0)
-    cos = float((y * ref).sum() / (np.linalg.norm(y) * np.linalg.norm(ref) + 1e-300)) if y.size else 1.0
-    assert err <= ATOL * scale, f"{tag}: max-abs {err:.3e} (scale {scale:.2f})"
-    assert cos >= COS, f"{tag}: cosine {cos:.7f}"
-    return err, cos
 
 
 def _rounded_layer(layer):

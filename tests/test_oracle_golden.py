@@ -107,3 +107,31 @@ def test_nan_quirk_matches_reference_semantics():
     r0 = O.apply_sere(ids, sim, 1, 0.0)
     np.testing.assert_array_equal(r0.new_indices, [[0, -1], [1, -1]])
     assert r0.reroute_map == {2: -1, 3: -1}
+
+
+def test_bf16_round_matches_torch():
+    """oracle.bf16_round (nearest-even via float32) equals torch's bfloat16 conversion."""
+    import torch
+
+    rng = np.random.default_rng(0)
+    a = np.concatenate([rng.standard_normal(100000) * s for s in (1e-3, 1.0, 37.0)])
+    a = np.concatenate([a, [0.0, -0.0, 1.0, 1.00390625, 1.0078125 + 2 ** -9, 65504.0]])
+    want = torch.as_tensor(a.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    np.testing.assert_array_equal(O.bf16_round(a), want)
+
+
+def test_block_forward_reduces_to_layer_chain():
+    """oracle.block_forward is the residual chain x += layer_forward(bf16(RMSNorm(x))) with the
+    given routes; S == K leaves the ids untouched."""
+    layers = O.gen_layers(1, 2, 8, 2, 16, 24, 1)
+    rng = np.random.default_rng(2)
+    x0 = rng.standard_normal((6, 16))
+    routes = [O.route_topk(l.w_router, 2, x0) for l in layers]
+    sims = [O.random_symmetric_sim(rng, 8) for _ in layers]
+    x, tr = O.block_forward(layers, x0, sims, 2, 0.5, routes)
+    want = x0.copy()
+    for l, layer in enumerate(layers):
+        h = O.bf16_round(O.rms_norm(want))
+        np.testing.assert_array_equal(tr[l]["final"], routes[l][0])
+        want = want + O.layer_forward(layer, h, routes[l][0], routes[l][1])
+    np.testing.assert_array_equal(x, want)
