@@ -201,6 +201,12 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
  * before touching shared data. 0 disables (plain stream order). */
 int sere_set_pdl(int enable);
 
+/* L2 prefetch of each layer's first FFN weights while re-routing and count/align run
+ * (helper CTAs of the align launch, `cp.async.bulk.prefetch.L2`): `bytes` per layer (0 =
+ * off), spread over `ctas` CTAs (<= 147); whole_experts = 1 prefetches gate/up AND down
+ * weights of each chosen expert, 0 only gate/up. Process-wide setting (tuning knob). */
+int sere_set_prefetch(int64_t bytes, int ctas, int whole_experts);
+
 /* Profiling hook: when n == 6, every following layer call on this host thread records
  * events[0..4] before its five stages (align, permute, gate/up GEMM, down GEMM,
  * combine) and events[5] after the last, on the launch stream (cudaEvent_t handles).

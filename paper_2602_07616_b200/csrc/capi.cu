@@ -191,6 +191,15 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.r_max = L.r_max;
   ap.ffn_ctas = sms;
   ap.dbg = g_align_dbg;
+  if (g_prefetch.budget > 0 && g_prefetch.ctas > 0) {
+    const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
+    ap.pf_w13 = w13;
+    ap.pf_w2 = w13 + bank_w13_bytes(L.Et, d);
+    ap.pf_w13_bytes = static_cast<long long>(bank_w13_bytes(1, d));
+    ap.pf_w2_bytes = static_cast<long long>(bank_w2_bytes(1, d));
+    ap.pf_budget = g_prefetch.budget;
+    ap.pf_whole = g_prefetch.whole;
+  }
   stage_mark(0, stream);
   cudaError_t e = launch_reroute_align(ap, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -227,6 +236,10 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 
 namespace sere {
 bool g_pdl = false;  // measured no gain on the C4 step; kept switchable (sere_set_pdl)
+#ifndef SERE_PREFETCH_MB
+#define SERE_PREFETCH_MB 64
+#endif
+PrefetchCfg g_prefetch = {static_cast<long long>(SERE_PREFETCH_MB) << 20, 32, 0};
 }  // namespace sere
 
 using namespace sere;
@@ -583,6 +596,14 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
     const cudaError_t e = launch_moe_ffn(fp, num_sms(), static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return SERE_ERR_CUDA;
   }
+  return SERE_OK;
+}
+
+int sere_set_prefetch(int64_t bytes, int ctas, int whole_experts) {
+  if (bytes < 0 || ctas < 0 || ctas > 147) return SERE_ERR_CONFIG;
+  g_prefetch.budget = bytes;
+  g_prefetch.ctas = ctas;
+  g_prefetch.whole = whole_experts != 0;
   return SERE_OK;
 }
 

@@ -34,7 +34,22 @@ struct AlignParams {
   int r_max;         // rows of the permuted batch buffer (row_token is staged in smem when it fits)
   int ffn_ctas;      // grid of the fused FFN (its first wave of gate/up units)
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
+  // L2 prefetch of the FFN's first weights (CTAs 1..pf_ctas of the align grid, see
+  // reroute_align.cu prefetch_role): bank regions of this layer, bytes to prefetch
+  const uint8_t* pf_w13;
+  const uint8_t* pf_w2;
+  long long pf_w13_bytes, pf_w2_bytes;  // per bank expert (each expert's region is contiguous)
+  long long pf_budget;                  // bytes to prefetch per layer (0 = off)
+  int pf_whole;                         // 1: whole experts (gate/up then down), 0: gate/up regions only
 };
+
+// process-wide prefetch setting (sere_set_prefetch)
+struct PrefetchCfg {
+  long long budget;
+  int ctas;
+  int whole;
+};
+extern PrefetchCfg g_prefetch;
 
 struct FfnParams {
   const uint8_t* w13;  // gate/up tiles (expert, mt, kt) at ((expert*tiles_gu+mt)*ktiles_gu+kt)*16KB

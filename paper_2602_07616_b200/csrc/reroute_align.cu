@@ -64,8 +64,64 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
+// ---------------------------------------------------------------- L2 prefetch role
+// The FFN of this layer cannot start before re-routing and count/align are done, and
+// both are latency-bound: HBM sits idle for their ~15-20 us. CTAs 1..P of the align grid
+// use that window to pull the weights the FFN will stream first into L2: the bank experts
+// that are certainly active -- shared experts, then the primary experts (slots < S, never
+// rewritten, rerouting.py:147,155-156), ordered by their slot-count descending like the
+// FFN's longest-first schedule -- up to `pf_budget` bytes, split evenly over the P CTAs as
+// 16 KB tiles (`cp.async.bulk.prefetch.L2`, fire-and-forget: no smem, no waiting).
+__device__ void prefetch_role(const AlignParams& p, unsigned char* smem) {
+  const int T = p.T, K = p.K, Et = p.m_local + p.n_shared;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int* cnt = reinterpret_cast<int*>(smem);  // [Et] sort key: slot count (shared experts: above any)
+  int* order = cnt + Et;                    // [Et] schedule position -> bank expert
+  __shared__ int s_n;
+  for (int i = tid; i < Et; i += nthr) cnt[i] = i < p.m_local ? 0 : 0x40000000;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  const int s_eff = p.S < K ? p.S : K;
+  for (int i = tid; i < T * s_eff; i += nthr) {
+    const int t = i / s_eff, k = i - t * s_eff;
+    const int el = __ldg(p.ids_in + static_cast<size_t>(t) * K + k) - p.e_lo;
+    if (el >= 0 && el < p.m_local) atomicAdd(&cnt[el], 1);
+  }
+  __syncthreads();
+  for (int e = tid; e < Et; e += nthr) {
+    const int key = cnt[e];
+    if (key == 0) continue;
+    int rank = 0;
+    for (int f = 0; f < Et; ++f) {
+      const int kf = cnt[f];
+      rank += (kf > key) | ((kf == key) & (f < e));
+    }
+    order[rank] = e;
+    atomicAdd(&s_n, 1);
+  }
+  __syncthreads();
+  const long long per = p.pf_w13_bytes + (p.pf_whole ? p.pf_w2_bytes : 0);
+  long long total = static_cast<long long>(s_n) * per;
+  if (total > p.pf_budget) total = p.pf_budget;
+  const long long tiles = total / kTileBytes;
+  const int q = blockIdx.x - 1, P = gridDim.x - 1;
+  const long long lo = tiles * q / P, hi = tiles * (q + 1) / P;
+  for (long long j = lo + tid; j < hi; j += nthr) {
+    const long long off = j * kTileBytes;
+    const int e = order[static_cast<int>(off / per)];
+    const long long w = off % per;
+    const uint8_t* src = w < p.pf_w13_bytes ? p.pf_w13 + e * p.pf_w13_bytes + w
+                                            : p.pf_w2 + e * p.pf_w2_bytes + (w - p.pf_w13_bytes);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(kTileBytes) : "memory");
+  }
+}
+
 __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (blockIdx.x > 0) {  // helper CTAs: L2 prefetch of the FFN's first weights
+    prefetch_role(p, smem);
+    return;
+  }
   const int T = p.T, K = p.K, M = p.M, S = p.S;
   const int TK = T * K, TB = (T + kTokBlk - 1) / kTokBlk;
   const int e_lo = p.e_lo, m_loc = p.m_local, Et = m_loc + p.n_shared;  // expert-parallel ownership
@@ -496,7 +552,8 @@ cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
   const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, p.r_max);
   static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
   if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
-  return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
+  const int grid = (p.pf_budget > 0 && p.pf_w13 != nullptr && (p.mode & MODE_ALIGN)) ? 1 + g_prefetch.ctas : 1;
+  return launch_pdl(g_pdl, reroute_align_kernel, dim3(grid), dim3(kAlignThreads), smem, stream, p);
 }
 
 size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }

@@ -115,15 +115,15 @@ def test_prenorm_block_c4_vs_fp64_oracle(cuda_device, mode, S, rho, beta, sim_ki
             assert res.final_active == tr[l]["active"], (tag, l)
         if l > 0:  # the residual stream entering layer l (= after layer l-1)
             check_close(rec[l][2].double().cpu().numpy(), tr[l]["x"], f"{tag} x after layer {l - 1}")
-        # the bf16 layer input h = bf16(RMSNorm(x)): from the identical step input (layer 0) at
-        # most one bf16 ulp apart (fp32 vs fp64 rsqrt may flip a rounding); later layers see
-        # a stream that already differs by ~1e-3, so h gets the cosine bar and one ulp at |h| < 4
+        # the fused residual + RMSNorm epilogue: the bf16 layer input equals bf16(RMSNorm(x)) of
+        # the device's own residual stream to within one bf16 ulp (fp32 vs fp64 rsqrt may flip
+        # a rounding); the stream itself is held to the oracle chain above
+        x_dev = rec[l][2].double().cpu().numpy()
+        h_want = O.bf16_round(O.rms_norm(x_dev))
         h = rec[l][3].double().cpu().numpy()
-        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(tr[l]["h"]), 2.0 ** -126))) - 7)
-        if l == 0:
-            assert np.all(np.abs(h - tr[l]["h"]) <= ulp), (tag, "h layer 0")
-        else:
-            check_close(h, tr[l]["h"], f"{tag} h into layer {l}", atol=2.0 ** -6 + 1e-2)
+        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(h_want), 2.0 ** -126))) - 7)
+        assert np.all(np.abs(h - h_want) <= ulp), (tag, l, float(np.abs(h - h_want).max()))
+        assert (h != h_want).mean() < 1e-3, (tag, l)
     check_close(step.x.double().cpu().numpy(), x_ref, f"{tag} x after layer {L - 1} (output)")
 
 
