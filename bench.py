@@ -62,10 +62,6 @@ def parse_args():
     ap.add_argument("--sim", choices=["uniform", "clustered"], default="uniform")
     ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
                     help="expert-parallel transport for N>1: peer-memory kernels (ep_p2p) or NCCL collectives (ep)")
-    ap.add_argument("--prefetch-mb", type=float, default=None,
-                    help="L2 prefetch budget per layer (sere_set_prefetch; default: the library's)")
-    ap.add_argument("--prefetch-ctas", type=int, default=32)
-    ap.add_argument("--prefetch-whole", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     a = ap.parse_args()
@@ -379,10 +375,7 @@ def run_ours(args, wl):
         import torch.distributed as dist
 
         dist.barrier()
-    from paper_2602_07616_b200 import _lib, decode, ep
-
-    if args.prefetch_mb is not None:
-        _lib.call("sere_set_prefetch", int(args.prefetch_mb * (1 << 20)), args.prefetch_ctas, args.prefetch_whole)
+    from paper_2602_07616_b200 import decode, ep
 
     T, L = wl["T"], wl["L"]
     if world > 1:

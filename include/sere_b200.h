@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SERE_ABI_VERSION 1
+#define SERE_ABI_VERSION 2
 
 /* status codes  (paper_2602_07616_b200/errors.py keeps the same numbers) */
 enum {
@@ -201,11 +201,6 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
  * before touching shared data. 0 disables (plain stream order). */
 int sere_set_pdl(int enable);
 
-/* L2 prefetch of each layer's first FFN weights while re-routing and count/align run
- * (helper CTAs of the align launch, `cp.async.bulk.prefetch.L2`): `bytes` per layer (0 =
- * off), spread over `ctas` CTAs (<= 147); whole_experts = 1 prefetches gate/up AND down
- * weights of each chosen expert, 0 only gate/up. Process-wide setting (tuning knob). */
-int sere_set_prefetch(int64_t bytes, int ctas, int whole_experts);
 
 /* Profiling hook: when n == 6, every following layer call on this host thread records
  * events[0..4] before its five stages (align, permute, gate/up GEMM, down GEMM,
@@ -227,10 +222,6 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf);
 /* Debug experiments on the fused FFN (outputs become INVALID): bit0 = skip the weight
  * copies, bit1 = skip the MMAs. 0 = normal operation. */
 int sere_debug_set_ffn_mode(int mode);
-/* Experiment: gate/up activation rows gathered from the layer input inside the fused FFN
- * (a gather warp, 16-B cp.async per row chunk) instead of the permute kernel. Results are
- * bit-identical; measured slower, so 0 (off) is the default. */
-int sere_debug_set_ffn_gather(int enable);
 /* Debug: router phase clocks (clock64) per CTA, dev_buf[cta * 8 + phase]. NULL disables. */
 int sere_debug_set_route_clocks(int64_t* dev_buf);
 /* Kernel-only timing: relaunch the fused expert FFN `reps` times on the plan and operands
@@ -317,6 +308,8 @@ typedef struct {
   int32_t plan_groups_off; /* int32 offsets (in elements) inside the plan block: */
   int32_t plan_group_expert_off, plan_group_row0_off, plan_group_rows_off;
   int32_t plan_counts_off, plan_unit_off_gu, plan_unit_off_dn;
+  size_t off_ids_final;  /* int32 [T*K] the (re-routed) table the layer runs on            */
+  size_t off_blk_prefix; /* u16 [ceil(T/32)][Et] cells of each bank expert in earlier token blocks */
 } sere_ws_layout;
 
 int sere_layer_workspace_layout(int T, int K, int M, int n_shared, int d_h, int d_m,

@@ -63,6 +63,8 @@ class WsLayout(ctypes.Structure):
         ("plan_counts_off", ctypes.c_int32),
         ("plan_unit_off_gu", ctypes.c_int32),
         ("plan_unit_off_dn", ctypes.c_int32),
+        ("off_ids_final", ctypes.c_size_t),
+        ("off_blk_prefix", ctypes.c_size_t),
     ]
 
 
@@ -107,17 +109,15 @@ SIGNATURES = {
     "sere_debug_set_align_clocks": (_c_int, [_p]),
     "sere_debug_set_ffn_trace": (_c_int, [_p]),
     "sere_debug_set_ffn_mode": (_c_int, [_c_int]),
-    "sere_debug_set_ffn_gather": (_c_int, [_c_int]),
     "sere_debug_set_route_clocks": (_c_int, [_p]),
     "sere_set_pdl": (_c_int, [_c_int]),
-    "sere_set_prefetch": (_c_int, [ctypes.c_int64, _c_int, _c_int]),
     "sere_debug_replay_ffn": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_size,
                                        _c_int, _p]),
     "sere_layer_workspace_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                              ctypes.POINTER(WsLayout)]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lock = threading.Lock()
 _lib = None

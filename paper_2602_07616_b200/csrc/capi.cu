@@ -37,16 +37,6 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 long long* g_align_dbg = nullptr;  // sere_debug_set_align_clocks
 unsigned long long* g_ffn_trace = nullptr;  // sere_debug_set_ffn_trace
 int g_ffn_dbg_mode = 0;                     // sere_debug_set_ffn_mode
-#ifndef SERE_GATHER_X
-#define SERE_GATHER_X 0
-#endif
-// gather mode: the FFN's gather warp reads gate/up activation rows from x via row_token,
-// replacing the permute kernel and x_pack (FfnParams::gather). Bit-identical results, but
-// measured 45% slower FFN (99 -> 143 us on a 56-active C4 layer): one warp's 16-B cp.async
-// stream cannot keep up with the weight stream, so it is off (sere_debug_set_ffn_gather)
-bool g_ffn_gather = SERE_GATHER_X != 0;
-const void* g_last_x = nullptr;  // the last layer input (sere_debug_replay_ffn in gather mode)
-
 constexpr int kStageEvents = 6;
 thread_local cudaEvent_t t_stage_events[kStageEvents];
 thread_local bool t_stage_events_on = false;
@@ -64,7 +54,7 @@ inline void stage_mark(int i, cudaStream_t stream) {
 }
 
 struct WsLayout {
-  size_t plan, slot_row, row_token, x_pack, h_pack, y_perm, total;
+  size_t plan, slot_row, row_token, x_pack, h_pack, y_perm, ids_final, blk_prefix, total;
   int r_max;
   Dims d;
   int Et;
@@ -76,6 +66,7 @@ WsLayout ws_layout(int T, int K, int M, int n_shared, int d_h, int d_m) {
   L.Et = M + n_shared;
   L.r_max = round_up(T * (K + n_shared) + kRowAlign * L.Et, 8);
   const PlanOffsets po = plan_offsets(L.Et);
+  const int TB = (T + kTokBlkPerm - 1) / kTokBlkPerm;
   size_t off = 0;
   L.plan = off;
   off = align_up(off + static_cast<size_t>(po.total) * 4, 1024);
@@ -89,6 +80,10 @@ WsLayout ws_layout(int T, int K, int M, int n_shared, int d_h, int d_m) {
   off = align_up(off + static_cast<size_t>(L.d.ktiles_dn) * L.r_max * 128, 1024);
   L.y_perm = off;
   off = align_up(off + static_cast<size_t>(L.d.ksplit_dn) * L.r_max * L.d.d_h_pad * 4, 1024);
+  L.ids_final = off;
+  off = align_up(off + static_cast<size_t>(T) * K * 4, 1024);
+  L.blk_prefix = off;
+  off = align_up(off + static_cast<size_t>(round_up(TB * L.Et, 2)) * 2, 1024);
   L.total = off + 1024;  // slack for aligning the caller's base to 1024 B
   return L;
 }
@@ -138,9 +133,6 @@ FfnParams ffn_params(const void* bank, const WsLayout& L, uint8_t* ws, int activ
   fp.act = activation;
   fp.trace = g_ffn_trace;
   fp.dbg_mode = g_ffn_dbg_mode;
-  fp.row_token = reinterpret_cast<const int32_t*>(ws + L.row_token);
-  fp.x_row_bytes = L.d.d_h * 2;
-  fp.d_h = L.d.d_h;
   return fp;
 }
 
@@ -181,8 +173,9 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.n_active = n_active;
   ap.status_dev = status_dev;
   ap.plan = plan;
-  ap.slot_row = slot_row;
   ap.row_token = row_token;
+  ap.ids_final = reinterpret_cast<int32_t*>(ws + L.ids_final);
+  ap.blk_prefix = reinterpret_cast<uint16_t*>(ws + L.blk_prefix);
   ap.tiles_gu = d.tiles_gu;
   ap.tiles_dn = d.tiles_dn;
   ap.ksplit_dn = d.ksplit_dn;
@@ -191,32 +184,16 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.r_max = L.r_max;
   ap.ffn_ctas = sms;
   ap.dbg = g_align_dbg;
-  if (g_prefetch.budget > 0 && g_prefetch.ctas > 0) {
-    const uint8_t* w13 = reinterpret_cast<const uint8_t*>(bank);
-    ap.pf_w13 = w13;
-    ap.pf_w2 = w13 + bank_w13_bytes(L.Et, d);
-    ap.pf_w13_bytes = static_cast<long long>(bank_w13_bytes(1, d));
-    ap.pf_w2_bytes = static_cast<long long>(bank_w2_bytes(1, d));
-    ap.pf_budget = g_prefetch.budget;
-    ap.pf_whole = g_prefetch.whole;
-  }
   stage_mark(0, stream);
   cudaError_t e = launch_reroute_align(ap, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   stage_mark(1, stream);
-  const bool gather = g_ffn_gather && d_h % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  if (!gather) {
-    e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, row_token, L.r_max, x_pack, sms, stream);
-    if (e != cudaSuccess) return SERE_ERR_CUDA;
-  }
+  e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, L.Et, m_local, e_lo, ap.ids_final,
+                     ap.blk_prefix, T, K, n_shared, slot_row, row_token, L.r_max, x_pack, stream);
+  if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   FfnParams fp = ffn_params(bank, L, ws, activation);
-  if (gather) {
-    fp.gather = 1;
-    fp.x = reinterpret_cast<const uint8_t*>(x);
-    g_last_x = x;
-  }
   stage_mark(2, stream);
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -236,10 +213,6 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 
 namespace sere {
 bool g_pdl = false;  // measured no gain on the C4 step; kept switchable (sere_set_pdl)
-#ifndef SERE_PREFETCH_MB
-#define SERE_PREFETCH_MB 64
-#endif
-PrefetchCfg g_prefetch = {static_cast<long long>(SERE_PREFETCH_MB) << 20, 32, 0};
 }  // namespace sere
 
 using namespace sere;
@@ -341,6 +314,8 @@ int sere_layer_workspace_layout(int T, int K, int M, int n_shared, int d_h, int 
   out->off_x_pack = L.x_pack;
   out->off_h_pack = L.h_pack;
   out->off_y_perm = L.y_perm;
+  out->off_ids_final = L.ids_final;
+  out->off_blk_prefix = L.blk_prefix;
   out->total_bytes = L.total;
   out->r_max = L.r_max;
   out->d_h_pad = L.d.d_h_pad;
@@ -574,12 +549,6 @@ int sere_debug_set_ffn_trace(uint64_t* dev_buf) {
   return SERE_OK;
 }
 
-int sere_debug_set_ffn_gather(int enable) {
-  g_ffn_gather = enable != 0;
-  if (!g_ffn_gather) g_last_x = nullptr;
-  return SERE_OK;
-}
-
 int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_m, int activation, int T, int K,
                           void* workspace, size_t workspace_bytes, int reps, void* stream) {
   int rc = check_layer_shapes(M, n_shared, d_h, d_m, activation, T, K);
@@ -588,22 +557,10 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
   const WsLayout L = ws_layout(T, K, M, n_shared, d_h, d_m);
   if (workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
   FfnParams fp = ffn_params(bank, L, ws_base(workspace), activation);
-  if (g_ffn_gather && g_last_x != nullptr && d_h % 8 == 0) {
-    fp.gather = 1;
-    fp.x = reinterpret_cast<const uint8_t*>(g_last_x);
-  }
   for (int i = 0; i < reps; ++i) {
     const cudaError_t e = launch_moe_ffn(fp, num_sms(), static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return SERE_ERR_CUDA;
   }
-  return SERE_OK;
-}
-
-int sere_set_prefetch(int64_t bytes, int ctas, int whole_experts) {
-  if (bytes < 0 || ctas < 0 || ctas > 147) return SERE_ERR_CONFIG;
-  g_prefetch.budget = bytes;
-  g_prefetch.ctas = ctas;
-  g_prefetch.whole = whole_experts != 0;
   return SERE_OK;
 }
 

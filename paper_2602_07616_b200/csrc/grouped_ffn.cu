@@ -69,9 +69,7 @@ constexpr int kEpiGroups = kEpiWarps / 4;   // warp groups splitting a unit's 16
 // N = 96 with two issuers), so two issuers interleave their issue chains
 constexpr int kMmaWarps = SERE_MMA_WARPS;
 constexpr int kEpiWarp0 = 1 + kMmaWarps;
-constexpr int kGatherWarp = kEpiWarp0 + kEpiWarps;  // gate/up activation rows (gather mode)
-constexpr int kFfnThreads = 32 * (1 + kMmaWarps + kEpiWarps + 1);
-constexpr int kGatherArrivals = 32;  // full-barrier arrivals of the gather warp per k-step
+constexpr int kFfnThreads = 32 * (1 + kMmaWarps + kEpiWarps);
 constexpr int kPdlPrefetch = 4;
 #ifndef SERE_DEP_DEFER
 #define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
@@ -98,8 +96,6 @@ struct __align__(16) FfnSmemTail {
   int32_t queue[kQueue];
   int32_t e_page[kEntries], e_np[kEntries];  // producer: pages held by in-flight k-steps
   int32_t t_col[kMmaWarps][kTq], t_need[kMmaWarps][kTq];  // MMA: TMEM columns of in-flight units
-  int32_t g_page[kEntries], g_np[kEntries];  // gather warp: its copy of the page bookkeeping
-  int32_t tok[kColBlock];                    // gather warp: source token of each row of the unit
   uint32_t tmem_base;
   int32_t n_groups, units_gu, units_dn;
 };
@@ -189,13 +185,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kEntries; ++i) {
-      mbar_init(&tail->full[i], 1 + (p.gather ? kGatherArrivals : 0));
+      mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], kMmaWarps);
     }
     for (int i = 0; i < kTq; ++i) { mbar_init(&tail->tfull[i], kMmaWarps); mbar_init(&tail->tempty[i], kEpiWarps); }
     for (int i = 0; i < kQueue; ++i) {
       mbar_init(&tail->q_full[i], 1);
-      mbar_init(&tail->q_empty[i], kMmaWarps + kEpiWarps + 1);
+      mbar_init(&tail->q_empty[i], kMmaWarps + kEpiWarps);
     }
     fence_mbar_init();
     tail->n_groups = ng;
@@ -321,8 +317,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           ut[2] = globaltimer_ns();
         }
         const int bpk = ktile_bpages(U);
-        const bool gx = p.gather && !U.dn;  // activation rows come from the gather warp
-        const uint32_t b_bytes = gx ? 0u : static_cast<uint32_t>(U.n_mma) * 128u;
+        const uint32_t b_bytes = static_cast<uint32_t>(U.n_mma) * 128u;
         for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
           const int nk = min(kKT, U.kt_end - kt);
           const int np = kstep_pages(U, nk), bp = nk * bpk;
@@ -362,7 +357,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           }
           const bool gated = !pdl_done || dep_g >= 0;
           if (gated && n_pend + nk > kPdlPrefetch) pdl_flush();
-          for (int kk = 0; kk < (gx ? 0 : nk); ++kk) {
+          for (int kk = 0; kk < nk; ++kk) {
             uint8_t* bdst = pg + kk * bpk * kPageBytes;
             const uint8_t* bsrc = b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128;
             if (pdl_done && dep_g < 0) {
@@ -434,7 +429,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u,
                           acc_full ? (U.dn ? &w_full_dn : acc_full) : nullptr);
           nks_dn += U.dn;
-          if (p.gather) fence_proxy_async_shared_cta();  // gathered rows are generic-proxy (cp.async) writes
           tc_fence_after();
           const uint32_t pg_addr = smem_u32(smem + head * kPageBytes);
           if (!(p.dbg_mode & 2)) {
@@ -463,76 +457,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         if (tr && iter < kFfnTraceUnits) tr[1280 + iter] = globaltimer_ns();  // last MMA issued
       }
     }
-  } else if (warp == kGatherWarp) {
-    // ===================== gather warp (gather mode): for every gate/up k-step, the unit's
-    // activation tile [n_mma rows][64 k] is assembled in its B pages straight from x rows
-    // (row_token; -1 = padding -> zeros), 16-B cp.async per (row, chunk) at the SW128
-    // swizzled position, each lane then arrives on the k-step's full barrier when its copies
-    // have landed. The page/entry sequence is recomputed exactly as the producer does.
-    int qs = 0, head = 0, kstep = 0, oldest = 0;
-    uint32_t qph = 0;
-    if (p.gather) pdl_wait();  // x and row_token come from the preceding kernels
-    for (;;) {
-      mbar_wait(&tail->q_full[qs], qph);
-      const int u = tail->queue[qs];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tail->q_empty[qs]);
-      if (++qs == kQueue) { qs = 0; qph ^= 1u; }
-      if (u < 0 || !p.gather) {
-        if (u < 0) break;
-        continue;
-      }
-      const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
-      const bool gx = !U.dn;
-      if (gx) {
-        for (int r = lane; r < U.n_mma; r += 32) tail->tok[r] = p.row_token[U.row0 + r];
-        __syncwarp();
-      }
-      const int bpk = ktile_bpages(U);
-      for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
-        const int nk = min(kKT, U.kt_end - kt);
-        const int np = kstep_pages(U, nk);
-        if (head + np > kPages) head = 0;
-        for (;;) {  // the producer's FIFO release rule, on the gather warp's own bookkeeping
-          bool busy = kstep - oldest >= kEntries;
-          for (int s2 = oldest; !busy && s2 < kstep; ++s2)
-            busy = ranges_overlap(head, np, tail->g_page[s2 % kEntries], tail->g_np[s2 % kEntries]);
-          if (!busy) break;
-          mbar_wait(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u);
-          ++oldest;
-        }
-        const int e = kstep % kEntries;
-        __syncwarp();
-        if (lane == 0) {
-          tail->g_page[e] = head;
-          tail->g_np[e] = np;
-        }
-        __syncwarp();
-        if (gx) {
-          const uint32_t pg = smem_u32(smem + head * kPageBytes);
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint32_t bdst = pg + kk * bpk * kPageBytes;
-            const int col0 = (kt + kk) * 64;
-            for (int i = lane; i < U.n_mma * 8; i += 32) {
-              const int r = i >> 3, c = i & 7;
-              const int t = tail->tok[r];
-              const int col = col0 + c * 8;
-              const int avail = t < 0 ? 0 : min(16, max(0, (p.d_h - col) * 2));
-              const uint8_t* src = p.x + (avail ? static_cast<size_t>(t) * p.x_row_bytes + col * 2 : 0);
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(bdst + r * 128 + ((c ^ (r & 7)) << 4)),
-                           "l"(src), "r"(avail)
-                           : "memory");
-            }
-          }
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&tail->full[e]))
-                       : "memory");
-        } else {
-          mbar_arrive(&tail->full[e]);
-        }
-        head += np;
-      }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
   } else {
     // ===================== epilogue warps -> TMEM lane quadrant q = warp % 4
     const int q = warp & 3;                    // TMEM lane quadrant of this warp

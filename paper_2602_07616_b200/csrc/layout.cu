@@ -103,63 +103,115 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 }
 
 // ------------------------------------------------------------------ permute
-// x_pack[kt][row][64] (128-B rows, chunk-swizzled) <- x[row_token[row]][64*kt .. +64].
-// One warp per permuted row: the source token is read once, then every lane keeps
-// kPermVec independent 16-B loads in flight before storing (a latency-bound gather).
-constexpr int kPermVec = 8;
+// The permutation and the gather of one layer (moe.py:303-307's per-expert `x[rows]`):
+// CTA (tb, j) owns token block tb (32 tokens) and the j-th 512-B slice of every row.
+//  1. warp 0 ranks the block's cells: lane = token, slots in order; the cells of bank
+//     expert e get consecutive rows erow0[e] + blk_prefix[tb][e] + (cells of e earlier in
+//     the block, by slot then token) -- the group order (token block, slot, token) the
+//     align kernel's prefixes describe; __match_any_sync groups the lanes of one expert;
+//  2. slice j == 0 writes slot_row[t,k] (combine) and its inverse row_token;
+//  3. every warp copies its tokens' slice once from x and stores it into each of the
+//     token's rows of x_pack[kt][row][128 B] (SW128 chunk swizzle), so a token row is read
+//     once per slice instead of once per slot.
+// Padding rows are not written: their FFN columns never reach an output.
+constexpr int kPermThreads = 256;
+constexpr int kPermMaxSlots = 64;       // K + n_shared (K <= 32, n_shared <= 31)
+constexpr int kPermMaxExperts = 320;    // bank experts + shared experts (capi.cu kMaxExperts + kMaxShared)
+constexpr int kPermTokPerWarp = kTokBlkPerm / (kPermThreads / 32);
 
-__global__ void __launch_bounds__(256) permute_kernel(const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad,
-                                                      const int32_t* __restrict__ plan,
-                                                      const int32_t* __restrict__ row_token, int r_max,
-                                                      uint8_t* __restrict__ x_pack) {
+__global__ void __launch_bounds__(kPermThreads) permute_kernel(
+    const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
+    int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
+    int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
+    uint8_t* __restrict__ x_pack) {
+  __shared__ int s_row[kPermMaxSlots][kTokBlkPerm];
+  __shared__ int s_run[kPermMaxExperts];
   pdl_wait();
   pdl_trigger();
   if (plan[P_STATUS] != 0) return;
-  const int total_rows = plan[P_TOTAL_ROWS];
-  const int cpr = d_h_pad / 8;  // 16-B chunks per row
-  const int lane = threadIdx.x & 31;
+  const int tb = blockIdx.x, j = blockIdx.y;
+  const int t0 = tb * kTokBlkPerm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nslot = K + n_shared;
+  const int32_t* erow0 = plan + plan_offsets(Et).erow0;
+  if (warp == 0) {
+    for (int e = lane; e < m_loc; e += 32) s_run[e] = 0;
+    __syncwarp();
+    const int t = t0 + lane;
+    const bool valid = t < T;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = 0; k < K; ++k) {
+      const int e = valid ? __ldg(ids_final + static_cast<size_t>(t) * K + k) : -1;
+      const int el = (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1;  // -1: another rank's expert (EP)
+      const unsigned m = __match_any_sync(0xffffffffu, el);
+      int r = -1, base = 0;
+      if (el >= 0) {
+        base = s_run[el];
+        r = __ldg(erow0 + el) + __ldg(blk_prefix + static_cast<size_t>(tb) * Et + el) + base + __popc(m & lt);
+      }
+      __syncwarp();
+      if (el >= 0 && lane == __ffs(m) - 1) s_run[el] = base + __popc(m);
+      __syncwarp();
+      s_row[k][lane] = r;
+    }
+    for (int s2 = 0; s2 < n_shared; ++s2)  // shared experts: every token, in token order
+      s_row[K + s2][lane] = valid ? __ldg(erow0 + m_loc + s2) + t : -1;
+  }
+  __syncthreads();
+  if (j == 0) {
+    for (int i = threadIdx.x; i < kTokBlkPerm * nslot; i += blockDim.x) {
+      const int slot = i / kTokBlkPerm, l = i - slot * kTokBlkPerm;
+      const int t = t0 + l;
+      if (t >= T) continue;
+      const int r = s_row[slot][l];
+      slot_row[slot < K ? static_cast<size_t>(t) * K + slot : static_cast<size_t>(T) * K + t * n_shared + (slot - K)] = r;
+      if (r >= 0) row_token[r] = t;
+    }
+  }
+  // gather: lane owns 16-B piece q of the slice; tokens loaded first (all in flight), then stored
+  const int cpr = d_h_pad / 8;  // 16-B pieces per row
+  const int q = j * 32 + lane;
+  if (q >= cpr) return;
+  const int kt = q >> 3, c = q & 7;
   const bool vec = (d_h & 7) == 0;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < total_rows; r += (gridDim.x * blockDim.x) >> 5) {
-    const int t = row_token[r];
-    for (int c0 = 0; c0 < cpr; c0 += 32 * kPermVec) {
-      uint4 v[kPermVec];
+  uint4 v[kPermTokPerWarp];
 #pragma unroll
-      for (int i = 0; i < kPermVec; ++i) {
-        const int ch = c0 + lane + 32 * i;
-        const int k0 = ch * 8;
-        v[i] = make_uint4(0u, 0u, 0u, 0u);
-        if (t >= 0 && ch < cpr && k0 < d_h) {
-          const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
-          if (vec) {
-            v[i] = __ldg(reinterpret_cast<const uint4*>(src));
-          } else {
-            alignas(16) __nv_bfloat16 tmp[8];
+  for (int i = 0; i < kPermTokPerWarp; ++i) {
+    const int l = warp * kPermTokPerWarp + i, t = t0 + l;
+    const int k0 = q * 8;
+    v[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (t < T && k0 < d_h) {
+      const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
+      if (vec) {
+        v[i] = __ldg(reinterpret_cast<const uint4*>(src));
+      } else {
+        alignas(16) __nv_bfloat16 tmp[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) tmp[q] = (k0 + q < d_h) ? src[q] : __float2bfloat16(0.f);
-            v[i] = *reinterpret_cast<uint4*>(tmp);
-          }
-        }
+        for (int e = 0; e < 8; ++e) tmp[e] = (k0 + e < d_h) ? src[e] : __float2bfloat16(0.f);
+        v[i] = *reinterpret_cast<uint4*>(tmp);
       }
+    }
+  }
+  uint8_t* dst_kt = x_pack + static_cast<size_t>(kt) * r_max * 128;
 #pragma unroll
-      for (int i = 0; i < kPermVec; ++i) {
-        const int ch = c0 + lane + 32 * i;
-        if (ch < cpr) {
-          const int kt = ch >> 3, c = ch & 7;
-          *reinterpret_cast<uint4*>(x_pack + (static_cast<size_t>(kt) * r_max + r) * 128 + sw128_chunk(c, r) * 16) =
-              v[i];
-        }
-      }
+  for (int i = 0; i < kPermTokPerWarp; ++i) {
+    const int l = warp * kPermTokPerWarp + i;
+    if (t0 + l >= T) continue;
+    for (int slot = 0; slot < nslot; ++slot) {
+      const int r = s_row[slot][l];
+      if (r >= 0) *reinterpret_cast<uint4*>(dst_kt + static_cast<size_t>(r) * 128 + sw128_chunk(c, r) * 16) = v[i];
     }
   }
 }
 
-cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, const int32_t* row_token,
-                           int r_max, uint8_t* x_pack, int num_sms, cudaStream_t stream) {
-  int blocks = (r_max + 7) / 8;  // one warp per row, 8 warps per CTA
-  if (blocks > num_sms * 8) blocks = num_sms * 8;
-  if (blocks < 1) blocks = 1;
-  return launch_pdl(g_pdl, permute_kernel, dim3(blocks), dim3(256), 0, stream, x, d.d_h, d.d_h_pad, plan, row_token,
-                    r_max, x_pack);
+cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
+                           const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
+                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  if (K + n_shared > kPermMaxSlots || Et > kPermMaxExperts) return cudaErrorInvalidValue;
+  const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
+  return launch_pdl(g_pdl, permute_kernel, grid, dim3(kPermThreads), 0, stream, x, d.d_h, d.d_h_pad, plan, Et, m_loc,
+                    e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack);
 }
 
 // ------------------------------------------------------------------ combine

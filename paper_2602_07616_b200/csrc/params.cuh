@@ -27,29 +27,15 @@ struct AlignParams {
   int32_t* status_dev;
   // align outputs
   int32_t* plan;
-  int32_t* slot_row;
-  int32_t* row_token;
+  int32_t* row_token;  // padding rows are marked -1 here; the permute writes the token rows
   int tiles_gu, tiles_dn, ksplit_dn;  // FFN geometry (work units: plan.cuh group_units_*)
   int e_lo, m_local; // expert-parallel ownership: bank holds global experts [e_lo, e_lo+m_local)
   int r_max;         // rows of the permuted batch buffer (row_token is staged in smem when it fits)
   int ffn_ctas;      // grid of the fused FFN (its first wave of gate/up units)
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
-  // L2 prefetch of the FFN's first weights (CTAs 1..pf_ctas of the align grid, see
-  // reroute_align.cu prefetch_role): bank regions of this layer, bytes to prefetch
-  const uint8_t* pf_w13;
-  const uint8_t* pf_w2;
-  long long pf_w13_bytes, pf_w2_bytes;  // per bank expert (each expert's region is contiguous)
-  long long pf_budget;                  // bytes to prefetch per layer (0 = off)
-  int pf_whole;                         // 1: whole experts (gate/up then down), 0: gate/up regions only
+  int32_t* ids_final;     // [T,K] the (re-routed) table the layer runs on (align mode; the permute reads it)
+  uint16_t* blk_prefix;   // [TB][Et] cells of bank expert e in token blocks before tb (align mode)
 };
-
-// process-wide prefetch setting (sere_set_prefetch)
-struct PrefetchCfg {
-  long long budget;
-  int ctas;
-  int whole;
-};
-extern PrefetchCfg g_prefetch;
 
 struct FfnParams {
   const uint8_t* w13;  // gate/up tiles (expert, mt, kt) at ((expert*tiles_gu+mt)*ktiles_gu+kt)*16KB
@@ -65,12 +51,6 @@ struct FfnParams {
   int dbg_mode;               // debug experiments (results invalid): bit0 skip weight copies, bit1 skip MMAs,
                               // bit2 skip the expert-output stores
   unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
-  // gather mode (gather != 0): gate/up activation tiles are gathered from the layer input
-  // x [T][d_h] bf16 through row_token by the FFN's gather warp (no permute kernel, no x_pack)
-  int gather;
-  const uint8_t* x;
-  const int32_t* row_token;
-  int x_row_bytes, d_h;
 };
 constexpr int kFfnTraceStride = 2048;
 constexpr int kFfnTraceUnits = 200;
@@ -159,8 +139,9 @@ cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);
 cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const __nv_bfloat16* wd, int count,
                         const Dims& d, int Et, int first, uint8_t* bank, int unpack, cudaStream_t stream);
-cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, const int32_t* row_token,
-                           int r_max, uint8_t* x_pack, int num_sms, cudaStream_t stream);
+cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
+                           const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
+                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream);
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,

@@ -20,8 +20,8 @@
 //   unit_off_gu/dn[Et+1]  prefix of work units over the schedule order
 //   dep[Et]               gate/up units finished per group (the down units of a group
 //                         wait for all of them); zeroed by align
-//   mw_gu[Et]             feature blocks per gate/up unit by schedule position (kMwGuMax;
-//                         SERE_TAIL_MW1: 1 for groups that miss the FFN's first wave)
+//   mw_gu[Et]             feature blocks per gate/up unit by schedule position (kMwGuMax)
+//   erow0[Et]             first permuted row of bank expert e's group (-1: no cells)
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -41,7 +41,7 @@ enum PlanIdx : int {
 };
 
 struct PlanOffsets {
-  int counts, group_expert, group_row0, group_rows, sched, unit_off_gu, unit_off_dn, dep, mw_gu, total;
+  int counts, group_expert, group_row0, group_rows, sched, unit_off_gu, unit_off_dn, dep, mw_gu, erow0, total;
 };
 
 __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
@@ -55,11 +55,13 @@ __host__ __device__ inline PlanOffsets plan_offsets(int Et) {
   o.unit_off_dn = o.unit_off_gu + Et + 1;
   o.dep = o.unit_off_dn + Et + 1;
   o.mw_gu = o.dep + Et;
-  o.total = o.mw_gu + Et;
+  o.erow0 = o.mw_gu + Et;
+  o.total = o.erow0 + Et;
   return o;
 }
 
 constexpr int kRowAlign = 16;     // group padding = MMA N granularity (M=128, cta_group::1)
+constexpr int kTokBlkPerm = 32;   // token block of the group row order (align prefixes, permute ranks)
 constexpr int kColBlock = 256;    // max MMA columns (tokens) per work unit
 constexpr int kTile = 64;         // K elements per 128-B swizzled row
 constexpr int kTileBytes = 16384; // 128 rows x 64 bf16

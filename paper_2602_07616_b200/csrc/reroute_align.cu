@@ -27,8 +27,7 @@
 namespace sere {
 
 constexpr int kAlignThreads = 1024;
-constexpr int kAlignWarps = kAlignThreads / 32;
-constexpr int kTokBlk = 32;  // tokens per warp block in the rank pass (lane = token)
+constexpr int kTokBlk = kTokBlkPerm;  // token block of the group row order (the permute ranks inside it)
 constexpr int kMaxGroupsSched = 320;  // >= max bank experts + shared experts (capi.cu kMaxExperts + kMaxShared)
 #define SERE_PHASE(i) do { if (p.dbg && threadIdx.x == 0) p.dbg[(i)] = clock64(); } while (0)
 
@@ -39,19 +38,20 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   b += static_cast<size_t>(TK) * 4;                   // s_ids
   b += static_cast<size_t>(M) * 4 * 2;                // s_map, s_list
   b += static_cast<size_t>(Et) * 4 * 4;               // s_cnt, s_row0, s_gpad, s_sched
-  b += static_cast<size_t>(kAlignWarps) * Et * 4;     // s_bm (per-warp token masks)
-  b += static_cast<size_t>(round_up(TK, 2)) * 2;      // s_rk
-  b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb
+  b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb (u16 pairs updated by 32-bit atomics)
   b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_need, s_cls
   return round_up(static_cast<int>(b), 16);
 }
 constexpr size_t kAlignSmemCap = 200 * 1024;
-// + the row -> token table staged in shared memory (written out coalesced) when it fits
-__host__ __device__ inline bool align_stage_rows(int T, int K, int M, int Et, int r_max) {
-  return r_max > 0 && align_smem_bytes(T, K, M, Et) + static_cast<size_t>(r_max) * 4 <= kAlignSmemCap;
+// the similarity matrix is staged into shared memory by one bulk copy at kernel start (it
+// lands while the ids are loaded and the secondaries found) when it fits
+__host__ __device__ inline bool align_stage_sim(int T, int K, int M, int Et) {
+  const size_t sim_bytes = static_cast<size_t>(M) * M * 8;
+  return sim_bytes % 16 == 0 && align_smem_bytes(T, K, M, Et) + sim_bytes <= kAlignSmemCap;
 }
-__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et, int r_max) {
-  return align_smem_bytes(T, K, M, Et) + (align_stage_rows(T, K, M, Et, r_max) ? static_cast<size_t>(r_max) * 4 : 0);
+__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et, bool reroute) {
+  return align_smem_bytes(T, K, M, Et) +
+         (reroute && align_stage_sim(T, K, M, Et) ? static_cast<size_t>(M) * M * 8 : 0);
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -64,64 +64,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
-// ---------------------------------------------------------------- L2 prefetch role
-// The FFN of this layer cannot start before re-routing and count/align are done, and
-// both are latency-bound: HBM sits idle for their ~15-20 us. CTAs 1..P of the align grid
-// use that window to pull the weights the FFN will stream first into L2: the bank experts
-// that are certainly active -- shared experts, then the primary experts (slots < S, never
-// rewritten, rerouting.py:147,155-156), ordered by their slot-count descending like the
-// FFN's longest-first schedule -- up to `pf_budget` bytes, split evenly over the P CTAs as
-// 16 KB tiles (`cp.async.bulk.prefetch.L2`, fire-and-forget: no smem, no waiting).
-__device__ void prefetch_role(const AlignParams& p, unsigned char* smem) {
-  const int T = p.T, K = p.K, Et = p.m_local + p.n_shared;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  int* cnt = reinterpret_cast<int*>(smem);  // [Et] sort key: slot count (shared experts: above any)
-  int* order = cnt + Et;                    // [Et] schedule position -> bank expert
-  __shared__ int s_n;
-  for (int i = tid; i < Et; i += nthr) cnt[i] = i < p.m_local ? 0 : 0x40000000;
-  if (tid == 0) s_n = 0;
-  __syncthreads();
-  const int s_eff = p.S < K ? p.S : K;
-  for (int i = tid; i < T * s_eff; i += nthr) {
-    const int t = i / s_eff, k = i - t * s_eff;
-    const int el = __ldg(p.ids_in + static_cast<size_t>(t) * K + k) - p.e_lo;
-    if (el >= 0 && el < p.m_local) atomicAdd(&cnt[el], 1);
-  }
-  __syncthreads();
-  for (int e = tid; e < Et; e += nthr) {
-    const int key = cnt[e];
-    if (key == 0) continue;
-    int rank = 0;
-    for (int f = 0; f < Et; ++f) {
-      const int kf = cnt[f];
-      rank += (kf > key) | ((kf == key) & (f < e));
-    }
-    order[rank] = e;
-    atomicAdd(&s_n, 1);
-  }
-  __syncthreads();
-  const long long per = p.pf_w13_bytes + (p.pf_whole ? p.pf_w2_bytes : 0);
-  long long total = static_cast<long long>(s_n) * per;
-  if (total > p.pf_budget) total = p.pf_budget;
-  const long long tiles = total / kTileBytes;
-  const int q = blockIdx.x - 1, P = gridDim.x - 1;
-  const long long lo = tiles * q / P, hi = tiles * (q + 1) / P;
-  for (long long j = lo + tid; j < hi; j += nthr) {
-    const long long off = j * kTileBytes;
-    const int e = order[static_cast<int>(off / per)];
-    const long long w = off % per;
-    const uint8_t* src = w < p.pf_w13_bytes ? p.pf_w13 + e * p.pf_w13_bytes + w
-                                            : p.pf_w2 + e * p.pf_w2_bytes + (w - p.pf_w13_bytes);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(kTileBytes) : "memory");
-  }
-}
-
 __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  if (blockIdx.x > 0) {  // helper CTAs: L2 prefetch of the FFN's first weights
-    prefetch_role(p, smem);
-    return;
-  }
   const int T = p.T, K = p.K, M = p.M, S = p.S;
   const int TK = T * K, TB = (T + kTokBlk - 1) / kTokBlk;
   const int e_lo = p.e_lo, m_loc = p.m_local, Et = m_loc + p.n_shared;  // expert-parallel ownership
@@ -132,27 +76,42 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   int32_t* s_row0 = s_cnt + Et;  // first permuted row of each bank expert's group
   int32_t* s_gpad = s_row0 + Et;  // padded rows of group g
   int32_t* s_sched = s_gpad + Et; // schedule order of the groups
-  uint32_t* s_bm = reinterpret_cast<uint32_t*>(s_sched + Et);         // [warps][Et]
-  uint16_t* s_rk = reinterpret_cast<uint16_t*>(s_bm + kAlignWarps * Et);  // [TK] rank inside token block
-  uint16_t* s_cntb = s_rk + round_up(TK, 2);                             // [TB][Et] counts -> prefixes
+  uint16_t* s_cntb = reinterpret_cast<uint16_t*>(s_sched + Et);  // [TB][Et] counts -> prefixes
   uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
   uint8_t* s_need = s_hflag + round_up(M, 4);
   uint8_t* s_cls = s_need + round_up(M, 4);
+  const double* s_sim = reinterpret_cast<const double*>(smem + align_smem_bytes(T, K, M, Et));
   __shared__ int s_err_id, s_err_sim, s_err_route, s_err_domain, s_nneed;
+  __shared__ __align__(8) uint64_t s_sim_bar;
 
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
   const bool reroute = (p.mode & MODE_REROUTE) != 0;
   const bool align = (p.mode & MODE_ALIGN) != 0;
   const int s_eff = S < K ? S : K;  // S == K: identity re-routing, every routed expert is primary
+  const bool stage_sim = reroute && S < K && align_stage_sim(T, K, M, Et) &&
+                         (reinterpret_cast<uintptr_t>(p.sim) & 15) == 0;
   auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
 
-  if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0; }
-  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
-  if (align) {
-    for (int i = tid; i < kAlignWarps * Et; i += nthr) s_bm[i] = 0u;
-    for (int i = tid; i < TB * Et; i += nthr) s_cntb[i] = 0;
+  if (tid == 0) {
+    s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0;
+    if (stage_sim) {  // one bulk copy of the whole matrix (<= 32 KB pieces), overlapped with phases 1-3
+      mbar_init(&s_sim_bar, 1);
+      fence_mbar_init();
+      const uint32_t bytes = static_cast<uint32_t>(M) * M * 8;
+      mbar_arrive_expect_tx(&s_sim_bar, bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768u) {
+        const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(smem_u32(s_sim) + off), "l"(reinterpret_cast<const uint8_t*>(p.sim) + off), "r"(n),
+                     "r"(smem_u32(&s_sim_bar))
+                     : "memory");
+      }
+    }
   }
+  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
+  if (align)
+    for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr) reinterpret_cast<uint32_t*>(s_cntb)[i] = 0u;
   __syncthreads();
   pdl_wait();  // ids come from the router; outputs are read by the previous layer's kernels
   pdl_trigger();
@@ -184,14 +143,17 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     if (bad) s_err_id = 1;
   }
   if (reroute && (p.flags & SERE_FLAG_CHECK_SIM)) {  // rerouting.py:115-116 (NaN passes, as there)
+    if (stage_sim) mbar_wait(&s_sim_bar, 0);
+    const double* sim = stage_sim ? s_sim : p.sim;
     for (int i = tid; i < M * M; i += nthr) {
-      const double s = p.sim[i];
-      if (s < 0.0 || s > 1.0) s_err_sim = 1;
+      const double v = sim[i];
+      if (v < 0.0 || v > 1.0) s_err_sim = 1;
     }
   }
   __syncthreads();
   SERE_PHASE(1);
   if (s_err_id || s_err_sim) {
+    if (stage_sim) mbar_wait(&s_sim_bar, 0);  // no bulk copy may still target this CTA's smem at exit
     if (tid == 0) {
       const int code = s_err_domain ? SERE_ERR_DOMAIN
                                     : s_err_id ? (reroute ? SERE_ERR_DIMENSION : SERE_ERR_ROUTING) : SERE_ERR_INPUT;
@@ -227,16 +189,19 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     __syncthreads();
     SERE_PHASE(3);
     // ---- per-secondary argmax over the primary set (rerouting.py:78-97,157-164): one 16-lane
-    // group per secondary u; every lane first issues all its loads of row u (independent, so
-    // they overlap), then compares ascending with strict '>' and the group reduces to the
-    // first maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
+    // group per secondary u over row u (staged in shared memory, else straight from global with
+    // all loads of the row in flight first); lanes compare ascending with strict '>' and the
+    // group reduces to the first maximum (larger value, then lower index) -- the ascending
+    // strict-'>' scan's answer.
     const int n_need = s_nneed;
+    if (stage_sim) mbar_wait(&s_sim_bar, 0);
+    const double* sim = stage_sim ? s_sim : p.sim;
     const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
     for (int base = 0; base < n_need; base += ngrp) {
       const int li = base + grp;
       const bool have = li < n_need;
       const int e = have ? s_list[li] : 0;
-      const double* row = p.sim + static_cast<size_t>(e) * M;
+      const double* row = sim + static_cast<size_t>(e) * M;
       double bs = -CUDART_INF;
       int bi = -1;
       if (have) {
@@ -245,7 +210,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int v = v0 + glane + 16 * j;
-            vals[j] = v < M ? __ldg(row + v) : 0.0;
+            vals[j] = v < M ? (stage_sim ? row[v] : __ldg(row + v)) : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -271,13 +236,20 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     }
     __syncthreads();
     SERE_PHASE(4);
-    // ---- rewrite the secondary cells (weights are never touched) + outputs
+  }
+
+  // ---- the final table: rewrite the secondary cells (weights are never touched),
+  // write it out, and count cells per (token block, bank expert) for the align below. One work
+  // item per (token, 4-slot quad): T * ceil(K/4) items keep all threads busy.
+  {
     bool bad = false;
     const bool vec_out = vec && (reinterpret_cast<uintptr_t>(p.ids_out) & 15) == 0;
-    // one work item per (token, 4-slot quad): T * ceil(K/4) items keep all threads busy
+    const bool vec_ws = vec && (reinterpret_cast<uintptr_t>(p.ids_final) & 15) == 0;
+    uint32_t* cntb32 = reinterpret_cast<uint32_t*>(s_cntb);
     const int nq = (K + 3) >> 2;
     for (int it = tid; it < T * nq; it += nthr) {
       const int t = it / nq, k0 = (it - t * nq) * 4;
+      const int tbE = (t / kTokBlk) * Et;
       int v4[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -285,21 +257,34 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         v4[j] = 0;
         if (k < K) {
           int e = s_ids[k * T + t];
-          if (k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
+          if (reroute && k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
             e = s_map[e];
-            s_ids[k * T + t] = e;
             bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
           }
           v4[j] = e;
+          if (align) {
+            const int el = local_of(e);
+            if (el >= 0) {
+              const int idx = tbE + el;
+              atomicAdd(cntb32 + (idx >> 1), 1u << (16 * (idx & 1)));
+            }
+          }
         }
       }
-      if (p.ids_out) {
+      if (reroute && p.ids_out) {
         int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
         if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
         else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
       }
+      if (align) {
+        int32_t* dst = p.ids_final + static_cast<size_t>(t) * K + k0;
+        if (vec_ws) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
+      }
     }
     if (bad) s_err_route = 1;
+  }
+  if (reroute) {
     if (p.expert_class)
       for (int e = tid; e < M; e += nthr) p.expert_class[e] = s_cls[e];
     if (p.reroute_map)
@@ -318,9 +303,9 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         if (p.plan) p.plan[P_NACTIVE] = base;
       }
     }
-    __syncthreads();
-    SERE_PHASE(5);
   }
+  __syncthreads();
+  SERE_PHASE(5);
 
   if (!align) {
     if (tid == 0 && p.status_dev) *p.status_dev = SERE_OK;
@@ -338,37 +323,11 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 
   // ================================================================ count/align
   // Rows of a group are ordered by (token block of 32, slot k, token): deterministic and
-  // computable without sorting. Pass 1, one warp per token block, lane = token: for each
-  // slot k every lane ORs its bit into the warp's mask of its expert; the cell's rank in
-  // the block is the block's running count of that expert + popc(mask & lanes below), and
-  // the lowest lane of each mask advances the running count. Counts never leave smem.
-  {
-    uint32_t* bm = s_bm + warp * Et;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int tb = warp; tb < TB; tb += nwarps) {
-      const int t = tb * kTokBlk + lane;
-      uint16_t* run = s_cntb + tb * Et;
-      for (int k = 0; k < K; ++k) {
-        const int el = t < T ? local_of(s_ids[k * T + t]) : -1;
-        if (el >= 0) atomicOr(&bm[el], 1u << lane);
-        __syncwarp();
-        unsigned m = 0;
-        if (el >= 0) {
-          m = bm[el];
-          s_rk[k * T + t] = static_cast<uint16_t>(run[el] + __popc(m & lt));
-        }
-        __syncwarp();
-        if (el >= 0 && lane == __ffs(m) - 1) {
-          run[el] = static_cast<uint16_t>(run[el] + __popc(m));
-          bm[el] = 0u;
-        }
-        __syncwarp();
-      }
-    }
-  }
-  __syncthreads();
-  SERE_PHASE(6);
-  // block counts -> exclusive prefixes over blocks; totals per bank expert
+  // computable without sorting. Here: block counts -> exclusive prefixes over blocks and
+  // totals per bank expert, the group layout, the FFN schedule. The rank of each cell inside
+  // its token block, the permutation (slot_row / row_token) and the gather of the token rows
+  // are the permute kernel's (many CTAs; layout.cu), which reads the prefixes from
+  // `blk_prefix` and the groups' first rows from the plan.
   for (int e = tid; e < Et; e += nthr) {
     if (e < m_loc) {
       int run = 0;
@@ -414,14 +373,18 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       int gb = 0, rb = 0;
       for (int w = 0; w < warp; ++w) { gb += s_tot[0][w]; rb += s_tot[1][w]; }
       if (e < Et) {
+        const int row0 = act ? rb + r_in - pad : -1;
         if (act) {
           plan[po.group_expert + gb + gi] = e;
-          plan[po.group_row0 + gb + gi] = rb + r_in - pad;
+          plan[po.group_row0 + gb + gi] = row0;
           plan[po.group_rows + gb + gi] = cnt;
           s_gpad[gb + gi] = pad;
+          // padding rows of the group carry no token (their FFN columns are never read)
+          for (int r = row0 + cnt; r < row0 + pad; ++r) p.row_token[r] = -1;
         }
-        s_row0[e] = act ? rb + r_in - pad : -1;
+        s_row0[e] = row0;
         plan[po.counts + e] = cnt;
+        plan[po.erow0 + e] = row0;
       }
       if (warp == nch - 1 && lane == 0) {
         const int g_tot = gb + s_tot[0][warp], r_tot = rb + s_tot[1][warp];
@@ -434,6 +397,9 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       }
     }
   }
+  // block prefixes out for the permute kernel (coalesced 32-bit words)
+  for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr)
+    reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
   __syncthreads();
   SERE_PHASE(10);
   // schedule order of the fused FFN: padded rows descending, ties by group index (a
@@ -456,25 +422,16 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
   __syncthreads();
   SERE_PHASE(11);
-  if (warp == nwarps - 1) {  // unit prefixes over the schedule order (a warp idle in pass 2 for T < 992)
-    int gu_base = 0, dn_base = 0, gu2_base = 0;
+  if (warp == nwarps - 1) {  // unit prefixes over the schedule order
+    int gu_base = 0, dn_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
       int ugu = 0, udn = 0;
       if (i < G) {
         ugu = s_ugu[i];
         udn = s_udn[i];
+        plan[po.mw_gu + i] = kMwGuMax;
       }
-#ifndef SERE_TAIL_MW1
-#define SERE_TAIL_MW1 0
-#endif
-      const int gu2_in = warp_incl_scan(ugu);
-      if (i < G) {
-        const int cap = (!SERE_TAIL_MW1 || gu2_base + gu2_in <= p.ffn_ctas) ? kMwGuMax : 1;
-        if (cap != kMwGuMax) ugu = group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, cap);
-        plan[po.mw_gu + i] = cap;
-      }
-      gu2_base += __shfl_sync(0xffffffffu, gu2_in, 31);
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {
         plan[po.unit_off_gu + i] = gu_base + gu_in - ugu;
@@ -488,72 +445,19 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       plan[P_UNITS_DN] = dn_base;
       plan[po.unit_off_gu + G] = gu_base;
       plan[po.unit_off_dn + G] = dn_base;
+      plan[P_STATUS] = SERE_OK;
+      if (p.status_dev) *p.status_dev = SERE_OK;
     }
   }
   SERE_PHASE(8);
-
-  // ---- pass 2: permuted row of every (token, slot) cell and its inverse. slot_row goes
-  // out as one vector store per token; row_token is assembled in shared memory and
-  // written out coalesced (a single SM cannot afford T*K scattered 4-B global stores)
-  const bool stage = align_stage_rows(T, K, M, Et, p.r_max);
-  int32_t* s_rt = reinterpret_cast<int32_t*>(smem + align_smem_bytes(T, K, M, Et));
-  int32_t* rt = stage ? s_rt : p.row_token;
-  const bool vec_sr = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(p.slot_row) & 15) == 0;
-  const int nq = (K + 3) >> 2;  // one work item per (token, 4-slot quad)
-  for (int it = tid; it < T * nq; it += nthr) {
-    const int t = it / nq, k0 = (it - t * nq) * 4;
-    const int tb = t / kTokBlk;
-    {
-      int rows4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int k = k0 + j;
-        rows4[j] = -1;  // -1: owned by another rank (expert parallelism), the combine skips it
-        if (k < K) {
-          const int el = local_of(s_ids[k * T + t]);
-          if (el >= 0) {
-            rows4[j] = s_row0[el] + s_cntb[tb * Et + el] + s_rk[k * T + t];
-            rt[rows4[j]] = t;
-          }
-        }
-      }
-      int32_t* dst = p.slot_row + static_cast<size_t>(t) * K + k0;
-      if (vec_sr) *reinterpret_cast<int4*>(dst) = make_int4(rows4[0], rows4[1], rows4[2], rows4[3]);
-      else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = rows4[j];
-    }
-  }
-  for (int it = tid; it < T * p.n_shared; it += nthr) {  // shared experts: every token, in token order
-    const int t = it / p.n_shared, s = it - t * p.n_shared;
-    const int row = s_row0[m_loc + s] + t;
-    p.slot_row[TK + t * p.n_shared + s] = row;
-    rt[row] = t;
-  }
-  for (int e = warp; e < Et; e += nwarps) {  // padding rows of each group
-    const int cnt = s_cnt[e];
-    if (cnt == 0) continue;
-    const int pad = round_up(cnt, kRowAlign);
-    if (lane < pad - cnt) rt[s_row0[e] + cnt + lane] = -1;
-  }
-  if (stage) {
-    __syncthreads();
-    const int R = plan[P_TOTAL_ROWS];
-    for (int i = tid * 4; i < R; i += nthr * 4) {  // R is a multiple of 16
-      *reinterpret_cast<int4*>(p.row_token + i) = *reinterpret_cast<const int4*>(s_rt + i);
-    }
-  }
-  if (tid == 0) {
-    plan[P_STATUS] = SERE_OK;
-    if (p.status_dev) *p.status_dev = SERE_OK;
-  }
-  SERE_PHASE(9);
 }
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
-  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, p.r_max);
+  const bool reroute = (p.mode & MODE_REROUTE) != 0;
+  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, reroute);
   static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
   if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
-  const int grid = (p.pf_budget > 0 && p.pf_w13 != nullptr && (p.mode & MODE_ALIGN)) ? 1 + g_prefetch.ctas : 1;
-  return launch_pdl(g_pdl, reroute_align_kernel, dim3(grid), dim3(kAlignThreads), smem, stream, p);
+  return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
 }
 
 size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }

@@ -58,15 +58,15 @@ def main() -> None:
     torch.cuda.synchronize()
     _lib.load().sere_debug_set_align_clocks(None)
     c = dbg.cpu().numpy()
-    names = {0: "init", 1: "load ids", 2: "need", 3: "list", 4: "argmax", 5: "rewrite+out", 6: "rank pass",
-             7: "block prefix", 10: "group layout", 11: "schedule sort", 8: "unit prefix", 9: "pass2 rows"}
-    order = [0, 1, 2, 3, 4, 5, 6, 7, 10, 11, 8, 9]
+    names = {0: "init", 1: "load ids", 2: "need", 3: "list", 4: "argmax", 5: "final table+counts",
+             7: "block prefix", 10: "group layout", 11: "schedule sort", 8: "unit prefix"}
+    order = [0, 1, 2, 3, 4, 5, 7, 10, 11, 8]
     prev = c[0]
     parts = []
     for i in order[1:]:
         parts.append(f"{names[i]} {int(c[i] - prev)}")
         prev = c[i]
-    print("reroute+align phase cycles:", ", ".join(parts), "| total", int(c[9] - c[0]))
+    print("reroute+align phase cycles:", ", ".join(parts), "| total", int(c[8] - c[0]))
 
 
 if __name__ == "__main__":

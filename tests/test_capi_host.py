@@ -48,7 +48,7 @@ def test_exports_are_extern_c(lib):
 def test_host_side_functions(lib):
     from paper_2602_07616_b200 import _lib
 
-    assert lib.sere_abi_version() == 1
+    assert lib.sere_abi_version() == _lib.ABI_VERSION == 2
     assert lib.sere_status_string(1) == b"ConfigError"
     assert lib.sere_status_string(4) == b"RoutingError"
     # bank bytes = E * 3 * d_h_pad * d_m_pad * 2 (bf16)

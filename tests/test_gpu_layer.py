@@ -275,29 +275,3 @@ def test_model_forward_teacher_forced_vs_oracle(cuda_device, layer_goldens):
         np.testing.assert_array_equal(res.layers[l].final.indices, tr[l]["final"])
         assert res.layers[l].active == tr[l]["active"]
     _check_close(res.output, y_ref, "model_forward")
-
-
-@pytest.mark.gpu
-def test_ffn_gather_mode_bit_identical(cuda_device):
-    """The experimental in-FFN activation gather (no permute kernel) computes exactly what the
-    permute + x_pack path computes."""
-    import torch
-
-    from paper_2602_07616_b200 import _lib
-    from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
-
-    model = DecodeModel(2, 32, 4, 512, 384, n_shared=1, seed=9, beta=1.0)
-    x0 = torch.randn(96, 512, device="cuda")
-    outs = []
-    for gather in (0, 1):
-        _lib.load().sere_debug_set_ffn_gather(gather)
-        try:
-            st = DecodeStep(model, 96, 1, 0.5)
-            st.set_input(x0)
-            st.run()
-            torch.cuda.synchronize()
-            st.check()
-            outs.append(st.x.clone())
-        finally:
-            _lib.load().sere_debug_set_ffn_gather(0)
-    assert torch.equal(outs[0], outs[1])
