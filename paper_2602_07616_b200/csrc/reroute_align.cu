@@ -42,17 +42,7 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_need, s_cls
   return round_up(static_cast<int>(b), 16);
 }
-constexpr size_t kAlignSmemCap = 200 * 1024;
-// the similarity matrix is staged into shared memory by one bulk copy at kernel start (it
-// lands while the ids are loaded and the secondaries found) when it fits
-__host__ __device__ inline bool align_stage_sim(int T, int K, int M, int Et) {
-  const size_t sim_bytes = static_cast<size_t>(M) * M * 8;
-  return sim_bytes % 16 == 0 && align_smem_bytes(T, K, M, Et) + sim_bytes <= kAlignSmemCap;
-}
-__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et, bool reroute) {
-  return align_smem_bytes(T, K, M, Et) +
-         (reroute && align_stage_sim(T, K, M, Et) ? static_cast<size_t>(M) * M * 8 : 0);
-}
+__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const int lane = lane_id();
@@ -80,35 +70,16 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
   uint8_t* s_need = s_hflag + round_up(M, 4);
   uint8_t* s_cls = s_need + round_up(M, 4);
-  const double* s_sim = reinterpret_cast<const double*>(smem + align_smem_bytes(T, K, M, Et));
   __shared__ int s_err_id, s_err_sim, s_err_route, s_err_domain, s_nneed;
-  __shared__ __align__(8) uint64_t s_sim_bar;
 
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
   const bool reroute = (p.mode & MODE_REROUTE) != 0;
   const bool align = (p.mode & MODE_ALIGN) != 0;
   const int s_eff = S < K ? S : K;  // S == K: identity re-routing, every routed expert is primary
-  const bool stage_sim = reroute && S < K && align_stage_sim(T, K, M, Et) &&
-                         (reinterpret_cast<uintptr_t>(p.sim) & 15) == 0;
   auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
 
-  if (tid == 0) {
-    s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0;
-    if (stage_sim) {  // one bulk copy of the whole matrix (<= 32 KB pieces), overlapped with phases 1-3
-      mbar_init(&s_sim_bar, 1);
-      fence_mbar_init();
-      const uint32_t bytes = static_cast<uint32_t>(M) * M * 8;
-      mbar_arrive_expect_tx(&s_sim_bar, bytes);
-      for (uint32_t off = 0; off < bytes; off += 32768u) {
-        const uint32_t n = bytes - off < 32768u ? bytes - off : 32768u;
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(smem_u32(s_sim) + off), "l"(reinterpret_cast<const uint8_t*>(p.sim) + off), "r"(n),
-                     "r"(smem_u32(&s_sim_bar))
-                     : "memory");
-      }
-    }
-  }
+  if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0; }
   for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
   if (align)
     for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr) reinterpret_cast<uint32_t*>(s_cntb)[i] = 0u;
@@ -143,17 +114,14 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     if (bad) s_err_id = 1;
   }
   if (reroute && (p.flags & SERE_FLAG_CHECK_SIM)) {  // rerouting.py:115-116 (NaN passes, as there)
-    if (stage_sim) mbar_wait(&s_sim_bar, 0);
-    const double* sim = stage_sim ? s_sim : p.sim;
     for (int i = tid; i < M * M; i += nthr) {
-      const double v = sim[i];
+      const double v = p.sim[i];
       if (v < 0.0 || v > 1.0) s_err_sim = 1;
     }
   }
   __syncthreads();
   SERE_PHASE(1);
   if (s_err_id || s_err_sim) {
-    if (stage_sim) mbar_wait(&s_sim_bar, 0);  // no bulk copy may still target this CTA's smem at exit
     if (tid == 0) {
       const int code = s_err_domain ? SERE_ERR_DOMAIN
                                     : s_err_id ? (reroute ? SERE_ERR_DIMENSION : SERE_ERR_ROUTING) : SERE_ERR_INPUT;
@@ -189,19 +157,16 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     __syncthreads();
     SERE_PHASE(3);
     // ---- per-secondary argmax over the primary set (rerouting.py:78-97,157-164): one 16-lane
-    // group per secondary u over row u (staged in shared memory, else straight from global with
-    // all loads of the row in flight first); lanes compare ascending with strict '>' and the
-    // group reduces to the first maximum (larger value, then lower index) -- the ascending
-    // strict-'>' scan's answer.
+    // group per secondary u; every lane first issues all its loads of row u (independent, so
+    // they overlap), then compares ascending with strict '>' and the group reduces to the
+    // first maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
     const int n_need = s_nneed;
-    if (stage_sim) mbar_wait(&s_sim_bar, 0);
-    const double* sim = stage_sim ? s_sim : p.sim;
     const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
     for (int base = 0; base < n_need; base += ngrp) {
       const int li = base + grp;
       const bool have = li < n_need;
       const int e = have ? s_list[li] : 0;
-      const double* row = sim + static_cast<size_t>(e) * M;
+      const double* row = p.sim + static_cast<size_t>(e) * M;
       double bs = -CUDART_INF;
       int bi = -1;
       if (have) {
@@ -210,7 +175,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int v = v0 + glane + 16 * j;
-            vals[j] = v < M ? (stage_sim ? row[v] : __ldg(row + v)) : 0.0;
+            vals[j] = v < M ? __ldg(row + v) : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -239,47 +204,49 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
 
   // ---- the final table: rewrite the secondary cells (weights are never touched),
-  // write it out, and count cells per (token block, bank expert) for the align below. One work
-  // item per (token, 4-slot quad): T * ceil(K/4) items keep all threads busy.
+  // write it out, and count the cells of each (token block, bank expert) for the align below.
+  // One warp per token block of 32 (lane = token), slots in order: a warp owns its block's row
+  // of counters, and __match_any_sync lets one lane add the cells of each expert.
   {
     bool bad = false;
     const bool vec_out = vec && (reinterpret_cast<uintptr_t>(p.ids_out) & 15) == 0;
     const bool vec_ws = vec && (reinterpret_cast<uintptr_t>(p.ids_final) & 15) == 0;
-    uint32_t* cntb32 = reinterpret_cast<uint32_t*>(s_cntb);
-    const int nq = (K + 3) >> 2;
-    for (int it = tid; it < T * nq; it += nthr) {
-      const int t = it / nq, k0 = (it - t * nq) * 4;
-      const int tbE = (t / kTokBlk) * Et;
-      int v4[4];
+    for (int tb = warp; tb < TB; tb += nwarps) {
+      const int t = tb * kTokBlk + lane;
+      const bool valid = t < T;
+      uint16_t* cnt_row = s_cntb + tb * Et;
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        int v4[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int k = k0 + j;
-        v4[j] = 0;
-        if (k < K) {
-          int e = s_ids[k * T + t];
-          if (reroute && k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
-            e = s_map[e];
-            bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
-          }
-          v4[j] = e;
-          if (align) {
-            const int el = local_of(e);
-            if (el >= 0) {
-              const int idx = tbE + el;
-              atomicAdd(cntb32 + (idx >> 1), 1u << (16 * (idx & 1)));
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + j;
+          int e = -1;
+          if (valid && k < K) {
+            e = s_ids[k * T + t];
+            if (reroute && k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
+              e = s_map[e];
+              bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
             }
           }
+          v4[j] = e;
+          if (align && k < K) {
+            const int el = valid ? local_of(e) : -1;
+            const unsigned m = __match_any_sync(0xffffffffu, el);
+            if (el >= 0 && lane == __ffs(m) - 1) cnt_row[el] = static_cast<uint16_t>(cnt_row[el] + __popc(m));
+            __syncwarp();
+          }
         }
-      }
-      if (reroute && p.ids_out) {
-        int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
-        if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
-        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
-      }
-      if (align) {
-        int32_t* dst = p.ids_final + static_cast<size_t>(t) * K + k0;
-        if (vec_ws) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
-        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
+        if (!valid) continue;
+        if (reroute && p.ids_out) {
+          int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
+          if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+          else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
+        }
+        if (align) {
+          int32_t* dst = p.ids_final + static_cast<size_t>(t) * K + k0;
+          if (vec_ws) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+          else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
+        }
       }
     }
     if (bad) s_err_route = 1;
@@ -379,8 +346,6 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
           plan[po.group_row0 + gb + gi] = row0;
           plan[po.group_rows + gb + gi] = cnt;
           s_gpad[gb + gi] = pad;
-          // padding rows of the group carry no token (their FFN columns are never read)
-          for (int r = row0 + cnt; r < row0 + pad; ++r) p.row_token[r] = -1;
         }
         s_row0[e] = row0;
         plan[po.counts + e] = cnt;
@@ -397,28 +362,35 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       }
     }
   }
-  // block prefixes out for the permute kernel (coalesced 32-bit words)
-  for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr)
-    reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
   __syncthreads();
   SERE_PHASE(10);
+  // block prefixes out for the permute kernel (coalesced 32-bit words); padding rows of every
+  // group carry no token (their FFN columns are never read): row_token = -1
+  for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr)
+    reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
+  for (int i = tid; i < Et * kRowAlign; i += nthr) {
+    const int e = i / kRowAlign, r = s_row0[e] + s_cnt[e] + (i - e * kRowAlign);
+    if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
+  }
   // schedule order of the fused FFN: padded rows descending, ties by group index (a
   // unit's cost grows with its column count, so this is longest-processing-time first)
   const int G = s_ngroups;
   __shared__ int s_ugu[kMaxGroupsSched], s_udn[kMaxGroupsSched];  // work units per schedule position
-  for (int g = tid; g < G; g += nthr) {
+  for (int g = warp; g < G; g += nwarps) {  // one warp per group: its rank by ballots over the keys
     const int key = s_gpad[g];
     int rank = 0;
-#pragma unroll 8
-    for (int j = 0; j < G; ++j) {
-      const int kj = s_gpad[j];
-      rank += (kj > key) | ((kj == key) & (j < g));
+    for (int j0 = 0; j0 < G; j0 += 32) {
+      const int j = j0 + lane;
+      const int kj = j < G ? s_gpad[j] : -1;
+      rank += __popc(__ballot_sync(0xffffffffu, (kj > key) | ((kj == key) & (j < g))));
     }
-    s_sched[rank] = g;
-    s_ugu[rank] = group_units_gu(key, p.tiles_gu);
-    s_udn[rank] = group_units_dn(key, p.tiles_dn, p.ksplit_dn);
-    plan[po.sched + rank] = g;
-    plan[po.dep + g] = 0;
+    if (lane == 0) {
+      s_sched[rank] = g;
+      s_ugu[rank] = group_units_gu(key, p.tiles_gu);
+      s_udn[rank] = group_units_dn(key, p.tiles_dn, p.ksplit_dn);
+      plan[po.sched + rank] = g;
+      plan[po.dep + g] = 0;
+    }
   }
   __syncthreads();
   SERE_PHASE(11);
@@ -453,8 +425,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 }
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
-  const bool reroute = (p.mode & MODE_REROUTE) != 0;
-  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared, reroute);
+  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared);
   static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
   if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);

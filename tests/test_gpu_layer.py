@@ -78,7 +78,10 @@ def test_layer_vs_oracle_small_configs(cuda_device, layer_goldens, name):
         res = O.apply_sere(ids, z[f"{name}_sims"][l], c["S"], c["rho"])
         ref2 = O.layer_forward(rl, x, res.new_indices, w, c["act"])
         _check_close(_run_layer(bank, x, res.new_indices, w, c["act"]), ref2, f"{name} sere layer {l}")
-        x = _bf16_round(ref)
+        # the next layer sees the RMS-normalised output (the benchmarked pre-norm block): the
+        # raw chain of these tiny-d_h configs grows to |y| ~ 18 (small_shared), where one bf16
+        # ulp of the kernel's bf16 intermediate h alone exceeds the absolute 1e-2 bar
+        x = _bf16_round(O.rms_norm(ref))
 
 
 def test_align_plan_integer_exact(cuda_device):
