@@ -105,10 +105,11 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 // ------------------------------------------------------------------ permute
 // The permutation and the gather of one layer (moe.py:303-307's per-expert `x[rows]`):
 // CTA (tb, j) owns token block tb (32 tokens) and the j-th 512-B slice of every row.
-//  1. warp 0 ranks the block's cells: lane = token, slots in order; the cells of bank
-//     expert e get consecutive rows erow0[e] + blk_prefix[tb][e] + (cells of e earlier in
-//     the block, by slot then token) -- the group order (token block, slot, token) the
-//     align kernel's prefixes describe; __match_any_sync groups the lanes of one expert;
+//  1. the block's cells are ranked: the cells of bank expert e get consecutive rows
+//     erow0[e] + blk_prefix[tb][e] + (cells of e earlier in the block, by slot then token) --
+//     the group order (token block, slot, token) the align kernel's prefixes describe. All
+//     slots at once: lane masks per (slot, expert) by shared-memory atomicOr, a prefix over
+//     slots of their popcounts, then rank = prefix + popc(mask & lanes below);
 //  2. slice j == 0 writes slot_row[t,k] (combine) and its inverse row_token;
 //  3. every warp copies its tokens' slice once from x and stores it into each of the
 //     token's rows of x_pack[kt][row][128 B] (SW128 chunk swizzle), so a token row is read
@@ -116,16 +117,22 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 // Padding rows are not written: their FFN columns never reach an output.
 constexpr int kPermThreads = 256;
 constexpr int kPermMaxSlots = 64;       // K + n_shared (K <= 32, n_shared <= 31)
-constexpr int kPermMaxExperts = 320;    // bank experts + shared experts (capi.cu kMaxExperts + kMaxShared)
 constexpr int kPermTokPerWarp = kTokBlkPerm / (kPermThreads / 32);
+
+__host__ __device__ inline size_t permute_smem_bytes(int K, int m_loc) {
+  return static_cast<size_t>(K) * m_loc * (4 + 2);  // lane masks u32 + slot prefixes u16, [K][m_loc]
+}
 
 __global__ void __launch_bounds__(kPermThreads) permute_kernel(
     const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
     int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
     int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
     uint8_t* __restrict__ x_pack) {
+  extern __shared__ __align__(16) uint8_t perm_smem[];
   __shared__ int s_row[kPermMaxSlots][kTokBlkPerm];
-  __shared__ int s_run[kPermMaxExperts];
+  uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem);            // [K][m_loc] lanes holding the expert
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] its cells at earlier slots
+  for (int i = threadIdx.x; i < K * m_loc; i += blockDim.x) s_bm[i] = 0u;
   pdl_wait();
   pdl_trigger();
   if (plan[P_STATUS] != 0) return;
@@ -134,29 +141,32 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nslot = K + n_shared;
   const int32_t* erow0 = plan + plan_offsets(Et).erow0;
-  if (warp == 0) {
-    for (int e = lane; e < m_loc; e += 32) s_run[e] = 0;
-    __syncwarp();
-    const int t = t0 + lane;
-    const bool valid = t < T;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int k = 0; k < K; ++k) {
-      const int e = valid ? __ldg(ids_final + static_cast<size_t>(t) * K + k) : -1;
-      const int el = (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1;  // -1: another rank's expert (EP)
-      const unsigned m = __match_any_sync(0xffffffffu, el);
-      int r = -1, base = 0;
-      if (el >= 0) {
-        base = s_run[el];
-        r = __ldg(erow0 + el) + __ldg(blk_prefix + static_cast<size_t>(tb) * Et + el) + base + __popc(m & lt);
-      }
-      __syncwarp();
-      if (el >= 0 && lane == __ffs(m) - 1) s_run[el] = base + __popc(m);
-      __syncwarp();
-      s_row[k][lane] = r;
-    }
-    for (int s2 = 0; s2 < n_shared; ++s2)  // shared experts: every token, in token order
-      s_row[K + s2][lane] = valid ? __ldg(erow0 + m_loc + s2) + t : -1;
+  const int t_lane = t0 + lane;
+  __syncthreads();
+  for (int k = warp; k < K; k += kPermThreads / 32) {  // warp = slot, lane = token
+    const int e = t_lane < T ? __ldg(ids_final + static_cast<size_t>(t_lane) * K + k) : -1;
+    const int el = (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1;  // -1: another rank's expert (EP)
+    s_row[k][lane] = el;
+    if (el >= 0) atomicOr(s_bm + k * m_loc + el, 1u << lane);
   }
+  __syncthreads();
+  for (int el = threadIdx.x; el < m_loc; el += blockDim.x) {
+    int run = 0;
+    for (int k = 0; k < K; ++k) {
+      s_pre[k * m_loc + el] = static_cast<uint16_t>(run);
+      run += __popc(s_bm[k * m_loc + el]);
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = warp; k < K; k += kPermThreads / 32) {
+    const int el = s_row[k][lane];
+    s_row[k][lane] = el < 0 ? -1
+                            : __ldg(erow0 + el) + __ldg(blk_prefix + static_cast<size_t>(tb) * Et + el) +
+                                  s_pre[k * m_loc + el] + __popc(s_bm[k * m_loc + el] & lt);
+  }
+  for (int s2 = warp; s2 < n_shared; s2 += kPermThreads / 32)  // shared experts: every token, in token order
+    s_row[K + s2][lane] = t_lane < T ? __ldg(erow0 + m_loc + s2) + t_lane : -1;
   __syncthreads();
   if (j == 0) {
     for (int i = threadIdx.x; i < kTokBlkPerm * nslot; i += blockDim.x) {
@@ -208,10 +218,13 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
                            const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
                            int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  if (K + n_shared > kPermMaxSlots || Et > kPermMaxExperts) return cudaErrorInvalidValue;
+  if (K + n_shared > kPermMaxSlots) return cudaErrorInvalidValue;
+  const size_t smem = permute_smem_bytes(K, m_loc);
+  static SmemAttrCache attr;
+  if (cudaError_t e = ensure_smem_attr(permute_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
-  return launch_pdl(g_pdl, permute_kernel, grid, dim3(kPermThreads), 0, stream, x, d.d_h, d.d_h_pad, plan, Et, m_loc,
-                    e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack);
+  return launch_pdl(g_pdl, permute_kernel, grid, dim3(kPermThreads), smem, stream, x, d.d_h, d.d_h_pad, plan, Et,
+                    m_loc, e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack);
 }
 
 // ------------------------------------------------------------------ combine

@@ -204,49 +204,48 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
 
   // ---- the final table: rewrite the secondary cells (weights are never touched),
-  // write it out, and count the cells of each (token block, bank expert) for the align below.
-  // One warp per token block of 32 (lane = token), slots in order: a warp owns its block's row
-  // of counters, and __match_any_sync lets one lane add the cells of each expert.
+  // write it out, and count the cells of each (token block, bank expert) for the align below
+  // (shared-memory atomics on u16 pairs). One work item per (token, 4-slot quad): T * ceil(K/4)
+  // items keep all threads busy.
   {
     bool bad = false;
     const bool vec_out = vec && (reinterpret_cast<uintptr_t>(p.ids_out) & 15) == 0;
     const bool vec_ws = vec && (reinterpret_cast<uintptr_t>(p.ids_final) & 15) == 0;
-    for (int tb = warp; tb < TB; tb += nwarps) {
-      const int t = tb * kTokBlk + lane;
-      const bool valid = t < T;
-      uint16_t* cnt_row = s_cntb + tb * Et;
-      for (int k0 = 0; k0 < K; k0 += 4) {
-        int v4[4];
+    uint32_t* cntb32 = reinterpret_cast<uint32_t*>(s_cntb);
+    const int nq = (K + 3) >> 2;
+    for (int it = tid; it < T * nq; it += nthr) {
+      const int t = it / nq, k0 = (it - t * nq) * 4;
+      const int tbE = (t / kTokBlk) * Et;
+      int v4[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + j;
-          int e = -1;
-          if (valid && k < K) {
-            e = s_ids[k * T + t];
-            if (reroute && k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
-              e = s_map[e];
-              bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
-            }
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        v4[j] = 0;
+        if (k < K) {
+          int e = s_ids[k * T + t];
+          if (reroute && k >= S && (s_cls[e] & SERE_CLASS_REROUTED)) {
+            e = s_map[e];
+            bad |= (e < 0 || e >= M);  // reference NaN quirk: a secondary mapped to -1
           }
           v4[j] = e;
-          if (align && k < K) {
-            const int el = valid ? local_of(e) : -1;
-            const unsigned m = __match_any_sync(0xffffffffu, el);
-            if (el >= 0 && lane == __ffs(m) - 1) cnt_row[el] = static_cast<uint16_t>(cnt_row[el] + __popc(m));
-            __syncwarp();
+          if (align) {
+            const int el = local_of(e);
+            if (el >= 0) {
+              const int idx = tbE + el;
+              atomicAdd(cntb32 + (idx >> 1), 1u << (16 * (idx & 1)));
+            }
           }
         }
-        if (!valid) continue;
-        if (reroute && p.ids_out) {
-          int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
-          if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
-          else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
-        }
-        if (align) {
-          int32_t* dst = p.ids_final + static_cast<size_t>(t) * K + k0;
-          if (vec_ws) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
-          else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
-        }
+      }
+      if (reroute && p.ids_out) {
+        int32_t* dst = p.ids_out + static_cast<size_t>(t) * K + k0;
+        if (vec_out) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
+      }
+      if (align) {
+        int32_t* dst = p.ids_final + static_cast<size_t>(t) * K + k0;
+        if (vec_ws) *reinterpret_cast<int4*>(dst) = make_int4(v4[0], v4[1], v4[2], v4[3]);
+        else for (int j = 0; j < 4 && k0 + j < K; ++j) dst[j] = v4[j];
       }
     }
     if (bad) s_err_route = 1;
@@ -364,37 +363,37 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
   __syncthreads();
   SERE_PHASE(10);
-  // block prefixes out for the permute kernel (coalesced 32-bit words); padding rows of every
-  // group carry no token (their FFN columns are never read): row_token = -1
-  for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr)
-    reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
-  for (int i = tid; i < Et * kRowAlign; i += nthr) {
-    const int e = i / kRowAlign, r = s_row0[e] + s_cnt[e] + (i - e * kRowAlign);
-    if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
-  }
   // schedule order of the fused FFN: padded rows descending, ties by group index (a
   // unit's cost grows with its column count, so this is longest-processing-time first)
   const int G = s_ngroups;
   __shared__ int s_ugu[kMaxGroupsSched], s_udn[kMaxGroupsSched];  // work units per schedule position
-  for (int g = warp; g < G; g += nwarps) {  // one warp per group: its rank by ballots over the keys
+  for (int g = tid; g < G; g += nthr) {
     const int key = s_gpad[g];
     int rank = 0;
-    for (int j0 = 0; j0 < G; j0 += 32) {
-      const int j = j0 + lane;
-      const int kj = j < G ? s_gpad[j] : -1;
-      rank += __popc(__ballot_sync(0xffffffffu, (kj > key) | ((kj == key) & (j < g))));
+#pragma unroll 8
+    for (int j = 0; j < G; ++j) {
+      const int kj = s_gpad[j];
+      rank += (kj > key) | ((kj == key) & (j < g));
     }
-    if (lane == 0) {
-      s_sched[rank] = g;
-      s_ugu[rank] = group_units_gu(key, p.tiles_gu);
-      s_udn[rank] = group_units_dn(key, p.tiles_dn, p.ksplit_dn);
-      plan[po.sched + rank] = g;
-      plan[po.dep + g] = 0;
-    }
+    s_sched[rank] = g;
+    s_ugu[rank] = group_units_gu(key, p.tiles_gu);
+    s_udn[rank] = group_units_dn(key, p.tiles_dn, p.ksplit_dn);
+    plan[po.sched + rank] = g;
+    plan[po.dep + g] = 0;
   }
   __syncthreads();
   SERE_PHASE(11);
-  if (warp == nwarps - 1) {  // unit prefixes over the schedule order
+  if (warp < nwarps - 1) {
+    // block prefixes out for the permute kernel (coalesced 32-bit words); padding rows of every
+    // group carry no token (their FFN columns are never read): row_token = -1
+    const int tid2 = tid, nthr2 = nthr - 32;
+    for (int i = tid2; i < round_up(TB * Et, 2) / 2; i += nthr2)
+      reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
+    for (int i = tid2; i < Et * kRowAlign; i += nthr2) {
+      const int e = i / kRowAlign, r = s_row0[e] + s_cnt[e] + (i - e * kRowAlign);
+      if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
+    }
+  } else {  // unit prefixes over the schedule order
     int gu_base = 0, dn_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
