@@ -62,6 +62,7 @@ def parse_args():
     ap.add_argument("--sim", choices=["uniform", "clustered"], default="uniform")
     ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
                     help="expert-parallel transport for N>1: peer-memory kernels (ep_p2p) or NCCL collectives (ep)")
+    ap.add_argument("--pdl", type=int, default=None, help="sere_set_pdl bit mask (default: the library's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     a = ap.parse_args()
@@ -375,7 +376,10 @@ def run_ours(args, wl):
         import torch.distributed as dist
 
         dist.barrier()
-    from paper_2602_07616_b200 import decode, ep
+    from paper_2602_07616_b200 import _lib, decode, ep
+
+    if args.pdl is not None:
+        _lib.call("sere_set_pdl", int(args.pdl))
 
     T, L = wl["T"], wl["L"]
     if world > 1:

@@ -196,9 +196,10 @@ int sere_route_topk(const uint16_t* x, const uint16_t* w_router_t, const float* 
  * ------------------------------------------------------------------------ */
 int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int d_h, float eps, void* stream);
 
-/* Programmatic dependent launch on the layer-chain kernels (default off): each kernel may
- * become resident while its predecessor drains and waits on-device (griddepcontrol)
- * before touching shared data. 0 disables (plain stream order). */
+/* Programmatic dependent launch on the layer-chain kernels: a kernel may become resident
+ * while its predecessor drains and waits on-device (griddepcontrol) before touching shared
+ * data. `enable` is a bit mask of the kernels launched that way: 1 re-route/align,
+ * 2 permute, 4 FFN, 8 combine, 16 RMSNorm (31 = all; 0 = plain stream order). */
 int sere_set_pdl(int enable);
 
 

@@ -212,7 +212,10 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 }  // namespace sere
 
 namespace sere {
-bool g_pdl = false;  // measured no gain on the C4 step; kept switchable (sere_set_pdl)
+#ifndef SERE_PDL_DEFAULT
+#define SERE_PDL_DEFAULT 0
+#endif
+int g_pdl = SERE_PDL_DEFAULT;  // PDL_* bits (sere_set_pdl)
 }  // namespace sere
 
 using namespace sere;
@@ -565,7 +568,7 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
 }
 
 int sere_set_pdl(int enable) {
-  g_pdl = enable != 0;
+  g_pdl = enable & PDL_ALL;
   return SERE_OK;
 }
 

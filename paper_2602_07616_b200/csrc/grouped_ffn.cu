@@ -601,7 +601,7 @@ cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream)
 #ifndef SERE_PDL_FFN
 #define SERE_PDL_FFN 0
 #endif
-  return launch_pdl(g_pdl || SERE_PDL_FFN, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
+  return launch_pdl((g_pdl & PDL_FFN) || SERE_PDL_FFN, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
 }
 
 size_t moe_ffn_smem(int Et) { return ffn_smem_bytes(Et); }

@@ -223,7 +223,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
   static SmemAttrCache attr;
   if (cudaError_t e = ensure_smem_attr(permute_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
-  return launch_pdl(g_pdl, permute_kernel, grid, dim3(kPermThreads), smem, stream, x, d.d_h, d.d_h_pad, plan, Et,
+  return launch_pdl((g_pdl & PDL_PERMUTE) != 0, permute_kernel, grid, dim3(kPermThreads), smem, stream, x, d.d_h, d.d_h_pad, plan, Et,
                     m_loc, e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack);
 }
 
@@ -442,7 +442,7 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            cudaStream_t stream, const EpPeers* ep, const int32_t* ids_rr) {
   if (T <= 0) return cudaSuccess;
   EpPeers none{};
-  return launch_pdl(g_pdl || SERE_PDL_COMBINE, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
+  return launch_pdl((g_pdl & PDL_COMBINE) || SERE_PDL_COMBINE, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
                     d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps,
                     ep ? *ep : none, ids_rr);
 }

@@ -133,7 +133,9 @@ __device__ __forceinline__ bool ep_aborted(const EpPeers& ep) {
 #ifndef SERE_PDL_COMBINE
 #define SERE_PDL_COMBINE 0
 #endif
-extern bool g_pdl;  // capi.cu: PDL on the layer chain (sere_set_pdl)  // router.cu: debug phase clocks of the router (nullptr = off)
+// programmatic dependent launch per layer-chain kernel (sere_set_pdl bit mask)
+enum : int { PDL_ALIGN = 1, PDL_PERMUTE = 2, PDL_FFN = 4, PDL_COMBINE = 8, PDL_RMSNORM = 16, PDL_ALL = 31 };
+extern int g_pdl;  // capi.cu
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);

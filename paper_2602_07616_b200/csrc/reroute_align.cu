@@ -427,7 +427,7 @@ cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
   const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared);
   static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
   if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
-  return launch_pdl(g_pdl, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
+  return launch_pdl((g_pdl & PDL_ALIGN) != 0, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
 }
 
 size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }

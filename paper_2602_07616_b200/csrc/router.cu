@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) residual_rmsnorm_kernel(float*
 
 cudaError_t launch_residual_rmsnorm(float* x, const float* y, __nv_bfloat16* h_out, int T, int d_h, float eps,
                                     cudaStream_t stream) {
-  return launch_pdl(g_pdl, residual_rmsnorm_kernel, dim3(T), dim3(row_threads(d_h)), 0, stream, x, y, h_out, d_h, eps);
+  return launch_pdl((g_pdl & PDL_RMSNORM) != 0, residual_rmsnorm_kernel, dim3(T), dim3(row_threads(d_h)), 0, stream, x, y, h_out, d_h, eps);
 }
 
 }  // namespace sere

@@ -142,7 +142,12 @@ def test_reference_model_dir_runs_on_gpu(cuda_device, tmp_path):
         np.testing.assert_array_equal(got.layers[l].final.indices, res.new_indices)
         y_ref = O.layer_forward(layers[l], rnd(xin), res.new_indices, w)
         y_dev = routed[l + 1][2] if l + 1 < L else got.output
-        check_close(y_dev, y_ref, f"reference-format model dir, layer {l} output")
+        # the raw reference chain (x <- MoE(x), gen_model weights) grows to |y| ~ 7.5 by layer 1;
+        # Appendix B's ideal bf16 kernel reaches 6.9e-3 at |y| ~ 4, so beyond |y| = 4 the bar
+        # keeps that relative accuracy (stated here, not in the shared helper: every BASELINE
+        # shape is held to the plain absolute 1e-2)
+        atol = 1e-2 * max(1.0, float(np.abs(y_ref).max()) / 4.0)
+        check_close(y_dev, y_ref, f"reference-format model dir, layer {l} output", atol=atol)
     io.save_model(model, tmp_path / "back")
     again = io.load_model(tmp_path / "back")
     for a, b in zip(model.layers, again.layers):
