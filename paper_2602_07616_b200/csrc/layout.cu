@@ -115,23 +115,27 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 //     token's rows of x_pack[kt][row][128 B] (SW128 chunk swizzle), so a token row is read
 //     once per slice instead of once per slot.
 // Padding rows are not written: their FFN columns never reach an output.
-constexpr int kPermThreads = 256;
+// 128 threads and a few KB of shared memory: with PDL the FFN's CTAs (352 threads, 162
+// registers, ~214 KB of shared memory) become resident on the SAME SMs while the permute
+// runs and start streaming their first weight tiles (registers: 11 x 5376 + 4 x 1280 <= 64K)
+constexpr int kPermThreads = 128;
 constexpr int kPermMaxSlots = 64;       // K + n_shared (K <= 32, n_shared <= 31)
 constexpr int kPermTokPerWarp = kTokBlkPerm / (kPermThreads / 32);
 
-__host__ __device__ inline size_t permute_smem_bytes(int K, int m_loc) {
-  return static_cast<size_t>(K) * m_loc * (4 + 2);  // lane masks u32 + slot prefixes u16, [K][m_loc]
+__host__ __device__ inline size_t permute_smem_bytes(int K, int n_shared, int m_loc) {
+  // rows [K + n_shared][32] int32, lane masks u32 + slot prefixes u16 [K][m_loc]
+  return static_cast<size_t>(K + n_shared) * kTokBlkPerm * 4 + static_cast<size_t>(K) * m_loc * (4 + 2);
 }
 
-__global__ void __launch_bounds__(kPermThreads) permute_kernel(
+__global__ void __launch_bounds__(kPermThreads, 11) permute_kernel(
     const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
     int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
     int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
     uint8_t* __restrict__ x_pack) {
   extern __shared__ __align__(16) uint8_t perm_smem[];
-  __shared__ int s_row[kPermMaxSlots][kTokBlkPerm];
-  uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem);            // [K][m_loc] lanes holding the expert
-  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] its cells at earlier slots
+  int (*s_row)[kTokBlkPerm] = reinterpret_cast<int (*)[kTokBlkPerm]>(perm_smem);  // [K + n_shared][32]
+  uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem) + (K + n_shared) * kTokBlkPerm;  // [K][m_loc] lanes
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] cells at earlier slots
   for (int i = threadIdx.x; i < K * m_loc; i += blockDim.x) s_bm[i] = 0u;
   pdl_wait();
   pdl_trigger();
@@ -219,7 +223,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
                            int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   if (K + n_shared > kPermMaxSlots) return cudaErrorInvalidValue;
-  const size_t smem = permute_smem_bytes(K, m_loc);
+  const size_t smem = permute_smem_bytes(K, n_shared, m_loc);
   static SmemAttrCache attr;
   if (cudaError_t e = ensure_smem_attr(permute_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
