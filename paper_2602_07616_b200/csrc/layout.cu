@@ -115,10 +115,9 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 //     token's rows of x_pack[kt][row][128 B] (SW128 chunk swizzle), so a token row is read
 //     once per slice instead of once per slot.
 // Padding rows are not written: their FFN columns never reach an output.
-// 128 threads and a few KB of shared memory: with PDL the FFN's CTAs (352 threads, 162
-// registers, ~214 KB of shared memory) become resident on the SAME SMs while the permute
-// runs and start streaming their first weight tiles (registers: 11 x 5376 + 4 x 1280 <= 64K)
-constexpr int kPermThreads = 128;
+// (128 threads capped at 46 registers, so that the PDL-launched FFN could co-reside, measured
+// 1.7% slower on the C4 step: the permute's own gather loses more than the FFN gains)
+constexpr int kPermThreads = 256;
 constexpr int kPermMaxSlots = 64;       // K + n_shared (K <= 32, n_shared <= 31)
 constexpr int kPermTokPerWarp = kTokBlkPerm / (kPermThreads / 32);
 
@@ -127,7 +126,7 @@ __host__ __device__ inline size_t permute_smem_bytes(int K, int n_shared, int m_
   return static_cast<size_t>(K + n_shared) * kTokBlkPerm * 4 + static_cast<size_t>(K) * m_loc * (4 + 2);
 }
 
-__global__ void __launch_bounds__(kPermThreads, 11) permute_kernel(
+__global__ void __launch_bounds__(kPermThreads) permute_kernel(
     const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
     int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
     int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
