@@ -242,7 +242,10 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
  *     All of them must be reachable from every rank (cudaIpcOpenMemHandle, see
  *     sere_ipc_*); sere_ep_peers lists every rank's pointers, entry `rank` = own.
  *     Per layer:  sere_route_topk_ep -> sere_ep_barrier -> sere_moe_ffn_ep ->
- *                 sere_ep_barrier -> sere_combine_ep.
+ *                 sere_ep_barrier -> sere_combine_ep,
+ *     or, with the fused barriers (peers->epoch != NULL), 3 calls and no barrier kernels:
+ *     the router's last CTA arrives, the re-route/align kernel of sere_moe_ffn_ep waits;
+ *     the FFN's last CTA arrives, the combine waits.
  * ------------------------------------------------------------------------ */
 #define SERE_MAX_EP_RANKS 8
 typedef struct {
@@ -257,6 +260,11 @@ typedef struct {
   int32_t* ids_all[SERE_MAX_EP_RANKS];
   float* w_all[SERE_MAX_EP_RANKS];
   int32_t* flags[SERE_MAX_EP_RANKS];
+  /* this rank's fused-barrier state; epoch == NULL: no fused barriers (call sere_ep_barrier) */
+  int32_t* epoch;    /* device epoch counter (zeroed once; shared with sere_ep_barrier)     */
+  int32_t* status;   /* device status word: SERE_ERR_CUDA after a timeout / abort           */
+  int32_t* arrivals; /* device counter of router CTAs (zeroed once)                          */
+  int64_t timeout_ns;
 } sere_ep_peers;
 
 /* Router for this rank's T_local = T_all/world tokens (x_local = own h_all rows
@@ -277,7 +285,8 @@ int sere_moe_ffn_ep(const void* bank, int M, int expert_lo, int expert_hi, int n
                     int activation, const double* sim, int S, double rho, int flags, const uint16_t* x_all,
                     const int32_t* ids_all, const float* w_all, int T_all, int K, int32_t* ids_out,
                     uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
-                    void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream);
+                    void* workspace, size_t workspace_bytes, int32_t* status_dev, const sere_ep_peers* peers,
+                    void* stream);
 /* Combine of this rank's tokens from the owners' expert outputs (peer loads), fixed slot
  * order: x_res[t] += y[t]; every rank's h_all row t0+t = bf16(RMSNorm(x_res[t])).
  * ids_rr = this rank's re-routed ids [T_all,K] (sere_moe_ffn_ep ids_out; identical on

@@ -38,6 +38,10 @@ class EpPeers(ctypes.Structure):
         ("ids_all", ctypes.c_void_p * MAX_EP_RANKS),
         ("w_all", ctypes.c_void_p * MAX_EP_RANKS),
         ("flags", ctypes.c_void_p * MAX_EP_RANKS),
+        ("epoch", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+        ("arrivals", ctypes.c_void_p),
+        ("timeout_ns", ctypes.c_int64),
     ]
 
 
@@ -94,7 +98,7 @@ SIGNATURES = {
     "sere_ep_barrier": (_c_int, [ctypes.POINTER(EpPeers), _p, _p, ctypes.c_int64, _p]),
     "sere_moe_ffn_ep": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_int,
                                  _c_double, _c_int, _p, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _c_size,
-                                 _p, _p]),
+                                 _p, ctypes.POINTER(EpPeers), _p]),
     "sere_combine_ep": (_c_int, [ctypes.POINTER(EpPeers), _p, _p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                                  _p, _p, ctypes.c_float, _p]),
     "sere_alloc_peer": (_c_int, [_c_size, ctypes.POINTER(ctypes.c_void_p)]),

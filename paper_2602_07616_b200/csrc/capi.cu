@@ -143,7 +143,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
               int T, int K, int32_t* ids_out, uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list,
               int32_t* n_active, float* y, uint16_t* y_bf16, void* workspace, size_t workspace_bytes,
               int32_t* status_dev, cudaStream_t stream, float* x_res = nullptr, uint16_t* h_next = nullptr,
-              float eps = 0.f, bool do_combine = true) {
+              float eps = 0.f, bool do_combine = true, const EpSync* sync = nullptr) {
   const WsLayout L = ws_layout(T, K, m_local, n_shared, d_h, d_m);
   if (workspace == nullptr || workspace_bytes < L.total) return SERE_ERR_WORKSPACE;
   if (bank == nullptr || x == nullptr || ids_in == nullptr || weights == nullptr)
@@ -176,6 +176,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   ap.row_token = row_token;
   ap.ids_final = reinterpret_cast<int32_t*>(ws + L.ids_final);
   ap.blk_prefix = reinterpret_cast<uint16_t*>(ws + L.blk_prefix);
+  if (sync != nullptr) ap.sync = *sync;
   ap.tiles_gu = d.tiles_gu;
   ap.tiles_dn = d.tiles_dn;
   ap.ksplit_dn = d.ksplit_dn;
@@ -194,6 +195,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   FfnParams fp = ffn_params(bank, L, ws, activation);
+  if (sync != nullptr) fp.sync = *sync;
   stage_mark(2, stream);
   e = launch_moe_ffn(fp, sms, stream);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
@@ -412,6 +414,8 @@ static int ep_peers(const sere_ep_peers* in, EpPeers* out) {
   std::memcpy(out, in, sizeof(EpPeers));
   for (int r = 0; r < in->world; ++r)
     if (!out->h_all[r] || !out->ids_all[r] || !out->w_all[r] || !out->flags[r]) return SERE_ERR_DIMENSION;
+  if (out->epoch != nullptr && (out->status == nullptr || out->arrivals == nullptr || out->timeout_ns <= 0))
+    return SERE_ERR_DIMENSION;
   return SERE_OK;
 }
 
@@ -446,7 +450,16 @@ int sere_moe_ffn_ep(const void* bank, int M, int expert_lo, int expert_hi, int n
                     int activation, const double* sim, int S, double rho, int flags, const uint16_t* x_all,
                     const int32_t* ids_all, const float* w_all, int T_all, int K, int32_t* ids_out,
                     uint8_t* expert_class, int32_t* reroute_map, int32_t* active_list, int32_t* n_active,
-                    void* workspace, size_t workspace_bytes, int32_t* status_dev, void* stream) {
+                    void* workspace, size_t workspace_bytes, int32_t* status_dev, const sere_ep_peers* peers,
+                    void* stream) {
+  EpSync sync{};
+  if (peers != nullptr) {
+    EpPeers ep;
+    const int rc = ep_peers(peers, &ep);
+    if (rc != SERE_OK) return rc;
+    if (ep.epoch == nullptr || ep.status == nullptr || ep.timeout_ns <= 0) return SERE_ERR_DIMENSION;
+    sync = ep_sync_of(ep);
+  }
   if (expert_lo < 0 || expert_hi > M || expert_hi < expert_lo) return SERE_ERR_DIMENSION;
   const int m_local = expert_hi - expert_lo;
   if (m_local + n_shared_local < 1) return SERE_ERR_DIMENSION;
@@ -459,7 +472,8 @@ int sere_moe_ffn_ep(const void* bank, int M, int expert_lo, int expert_hi, int n
   return run_layer(bank, M, expert_lo, m_local, n_shared_local, d_h, d_m, activation, sim, S, rho, flags,
                    MODE_REROUTE | MODE_ALIGN, x_all, ids_all, w_all, T_all, K, ids_out, expert_class, reroute_map,
                    active_list, n_active, nullptr, nullptr, workspace, workspace_bytes, status_dev,
-                   static_cast<cudaStream_t>(stream), nullptr, nullptr, 0.f, /*do_combine=*/false);
+                   static_cast<cudaStream_t>(stream), nullptr, nullptr, 0.f, /*do_combine=*/false,
+                   sync.world > 0 ? &sync : nullptr);
 }
 
 int sere_combine_ep(const sere_ep_peers* peers, const int32_t* ids_rr, const void* workspace, int M_local,

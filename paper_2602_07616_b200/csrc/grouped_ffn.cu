@@ -583,13 +583,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   tc_fence_after();
   if (tr && threadIdx.x == 0) { tr[7] = globaltimer_ns(); tr[814] = clock64(); }
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
-  if (threadIdx.x == 0 && status == 0) {  // last CTA out re-arms the plan's counters
-    __threadfence();
+  if (threadIdx.x == 0) {  // last CTA out re-arms the plan's counters (and, expert parallel, arrives)
+    if (p.sync.world > 0) __threadfence_system();  // this CTA's expert outputs, read by the peers
+    else __threadfence();
     if (atomicAdd(plan + P_DONE, 1) == static_cast<int>(gridDim.x) - 1) {
       for (int g = 0; g < ng; ++g) dep[g] = 0;
       plan[P_TICKET] = 0;
       plan[P_DONE] = 0;
       __threadfence();
+      if (p.sync.world > 0) ep_arrive(p.sync);
     }
   }
 }

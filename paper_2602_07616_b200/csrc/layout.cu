@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
     }
   } else {
     pdl_wait();  // peers' slot rows are ordered by the barrier kernel before us: wait for it
+    if (ep.epoch != nullptr) {  // fused barrier: every rank's expert outputs are final
+      __shared__ int s_ok;
+      if (threadIdx.x == 0) s_ok = ep_wait(ep_sync_dev(ep));
+      __syncthreads();
+      if (!s_ok) return;
+    }
     if (ep_aborted(ep)) return;  // a barrier timed out: no peer loads or stores on this step
     const int tg = ep.t0 + t, TK = ep.T_all * K;
     for (int k = threadIdx.x; k < nslot; k += blockDim.x) {

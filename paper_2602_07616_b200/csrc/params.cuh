@@ -12,6 +12,19 @@ namespace sere {
 enum : int { MODE_REROUTE = 1, MODE_ALIGN = 2 };
 enum : int { EPI_SWIGLU = 0, EPI_STORE_F32 = 1 };
 
+// Fused expert-parallel barrier (ep_p2p.cu): the kernel that ends a phase ARRIVES (its last
+// CTA bumps this rank's epoch and release-stores it into every rank's flag slot), the first
+// kernel of the next phase WAITS (one thread acquires every rank's slot >= its own epoch).
+// world == 0: no fused barrier.
+constexpr int kMaxEpRanks = 8;
+struct EpSync {
+  int world, rank;
+  int32_t* flags[kMaxEpRanks];  // every rank's flag words (kEpFlagWords each)
+  int32_t* epoch;               // this rank's epoch counter
+  int32_t* status;              // this rank's barrier status word (SERE_ERR_CUDA on timeout / abort)
+  long long timeout_ns;
+};
+
 struct AlignParams {
   const int32_t* ids_in;
   const double* sim;
@@ -35,6 +48,7 @@ struct AlignParams {
   long long* dbg;    // optional phase timestamps (sere_debug_set_align_clocks)
   int32_t* ids_final;     // [T,K] the (re-routed) table the layer runs on (align mode; the permute reads it)
   uint16_t* blk_prefix;   // [TB][Et] cells of bank expert e in token blocks before tb (align mode)
+  EpSync sync;            // expert parallel: wait for every rank's router rows before reading the table
 };
 
 struct FfnParams {
@@ -51,6 +65,7 @@ struct FfnParams {
   int dbg_mode;               // debug experiments (results invalid): bit0 skip weight copies, bit1 skip MMAs,
                               // bit2 skip the expert-output stores
   unsigned long long* trace;  // optional per-CTA unit timeline (sere_debug_set_ffn_trace), kFfnTraceStride u64 each
+  EpSync sync;                // expert parallel: the last CTA out arrives (expert outputs final)
 };
 constexpr int kFfnTraceStride = 2048;
 constexpr int kFfnTraceUnits = 200;
@@ -93,7 +108,6 @@ inline cudaError_t ensure_smem_attr(Kernel kernel, size_t smem, SmemAttrCache& c
 
 // Expert-parallel group seen through NVLink peer memory (ep_p2p.cu; world == 0: single GPU).
 // Every pointer array is indexed by rank; entry `rank` is this rank's own buffer.
-constexpr int kMaxEpRanks = 8;
 struct EpPeers {
   int world, rank;
   int t0, T_all;                      // this rank's first global token; tokens of the whole batch
@@ -105,7 +119,12 @@ struct EpPeers {
   __nv_bfloat16* h_all[kMaxEpRanks];  // rank r's gathered token states [T_all][d_h]
   int32_t* ids_all[kMaxEpRanks];      // rank r's gathered router ids [T_all][K]
   float* w_all[kMaxEpRanks];          // rank r's gathered router weights [T_all][K]
-  int32_t* flags[kMaxEpRanks];        // rank r's barrier flags [world]
+  int32_t* flags[kMaxEpRanks];        // rank r's barrier flags [kEpFlagWords]
+  // this rank's fused-barrier state (epoch == nullptr: no fused barriers, sere_ep_barrier instead)
+  int32_t* epoch;
+  int32_t* status;
+  int32_t* arrivals;                  // router CTAs done (the last one arrives)
+  long long timeout_ns;
 };
 
 // flags[r] holds kMaxEpRanks barrier slots followed by rank r's sticky ABORT word: a
@@ -124,6 +143,59 @@ __device__ __forceinline__ int ld_acquire_sys(const int32_t* p) {
 }
 __device__ __forceinline__ bool ep_aborted(const EpPeers& ep) {
   return ld_acquire_sys(ep.flags[ep.rank] + kEpAbortSlot) != 0;
+}
+__host__ __device__ inline EpSync ep_sync_dev(const EpPeers& ep) {
+  EpSync s{};
+  s.world = ep.world;
+  s.rank = ep.rank;
+  for (int r = 0; r < kMaxEpRanks; ++r) s.flags[r] = ep.flags[r];
+  s.epoch = ep.epoch;
+  s.status = ep.status;
+  s.timeout_ns = ep.timeout_ns;
+  return s;
+}
+inline EpSync ep_sync_of(const EpPeers& ep) {
+  EpSync s{};
+  if (ep.epoch == nullptr) return s;
+  s.world = ep.world;
+  s.rank = ep.rank;
+  for (int r = 0; r < kMaxEpRanks; ++r) s.flags[r] = ep.flags[r];
+  s.epoch = ep.epoch;
+  s.status = ep.status;
+  s.timeout_ns = ep.timeout_ns;
+  return s;
+}
+// one thread: this rank's writes so far (made system-visible by the caller's fences) are
+// published to every rank under a new epoch
+__device__ __forceinline__ void ep_arrive(const EpSync& s) {
+  __threadfence_system();
+  const int e = atomicAdd(s.epoch, 1) + 1;
+  for (int p = 0; p < s.world; ++p) st_release_sys(s.flags[p] + s.rank, e);
+}
+// one thread: wait until every rank arrived at this rank's current epoch; false on a timeout
+// (sticky abort raised on every rank) or when an abort is already raised
+__device__ __forceinline__ bool ep_wait(const EpSync& s) {
+  if (ld_acquire_sys(s.flags[s.rank] + kEpAbortSlot) != 0) {
+    if (s.status) atomicExch(s.status, 6 /* SERE_ERR_CUDA */);
+    return false;
+  }
+  const int e = *reinterpret_cast<volatile int32_t*>(s.epoch);
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int p = 0; p < s.world; ++p) {
+    while (ld_acquire_sys(s.flags[s.rank] + p) < e) {
+      __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > static_cast<unsigned long long>(s.timeout_ns)) {
+        if (s.status) atomicExch(s.status, 6 /* SERE_ERR_CUDA */);
+        for (int q = 0; q < s.world; ++q) st_release_sys(s.flags[q] + kEpAbortSlot, 1);
+        return false;
+      }
+    }
+  }
+  __threadfence();
+  return true;
 }
 
 // 1: the combine grid is launched with programmatic dependent launch and the FFN triggers

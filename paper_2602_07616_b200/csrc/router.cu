@@ -269,6 +269,23 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
   RC_PROBE(5);
 }
 
+// expert parallel with the fused barrier: every CTA counts itself out after its peer stores;
+// the last one arrives (its rows and every other CTA's are published under a new epoch)
+__device__ __forceinline__ void route_ep_arrive(const EpPeers& ep) {
+  if (ep.world == 0 || ep.epoch == nullptr || threadIdx.x != 0) return;
+  __threadfence_system();
+  const int total = static_cast<int>(gridDim.x * gridDim.y);
+  if (atomicAdd(ep.arrivals, 1) == total - 1) {
+    *ep.arrivals = 0;
+    EpSync s{};
+    s.world = ep.world;
+    s.rank = ep.rank;
+    for (int r = 0; r < kMaxEpRanks; ++r) s.flags[r] = ep.flags[r];
+    s.epoch = ep.epoch;
+    ep_arrive(s);
+  }
+}
+
 __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bfloat16* __restrict__ x,
                                                                    const __nv_bfloat16* __restrict__ wr,
                                                                    const float* __restrict__ bias, int T, int d_h,
@@ -364,6 +381,7 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
   }
   RC_PROBE(3);
   route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias, ids, weights, logits_out, dbg, ep);
+  route_ep_arrive(ep);
 }
 
 // tcgen05 variant (default for M <= 256, K chunk a multiple of 64): the experts are the MMA's
@@ -500,6 +518,7 @@ __global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat1
   }
   RC_PROBE(3);
   route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias, ids, weights, logits_out, dbg, ep, kRtTok);
+  route_ep_arrive(ep);
 }
 
 size_t route_workspace_bytes(int T, int d_h, int M) { return 256; }

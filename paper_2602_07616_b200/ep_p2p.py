@@ -121,7 +121,7 @@ class P2PDecodeStep(StageEvents):
     the same layer chain as `decode.DecodeStep`, whose output it reproduces bit for bit)."""
 
     def __init__(self, model, T: int, world: int, rank: int, retain_count: int = 1, threshold: float = 0.5,
-                 mode: str = "sere", eps: float = 1e-6, timeout_s: float = 5.0):
+                 mode: str = "sere", eps: float = 1e-6, timeout_s: float = 5.0, fused_barriers: bool = True):
         torch = _torch()
         self.model, self.T, self.world, self.rank, self.mode, self.eps = model, T, world, rank, mode, eps
         if not 1 <= world <= _lib.MAX_EP_RANKS:
@@ -146,6 +146,10 @@ class P2PDecodeStep(StageEvents):
         self.x = torch.zeros_like(self.x_in)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
         self.bar_status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.arrivals = torch.zeros(1, dtype=torch.int32, device=dev)
+        # fused barriers: the router's last CTA and the FFN's last CTA arrive, the align kernel and
+        # the combine wait (5 launches per layer); False: two sere_ep_barrier kernels (7 launches)
+        self.fused = bool(fused_barriers)
         self.route_ws = torch.zeros(max(_lib.load().sere_route_workspace_bytes(self.T_local, model.d_h, model.M), 1),
                                     dtype=torch.uint8, device=dev)
         self.outs = []
@@ -165,6 +169,7 @@ class P2PDecodeStep(StageEvents):
         # virtual ranks (one device): callbacks around the FFN launch, see connect_local
         self._ffn_pre = None
         self._ffn_post = None
+        self._combine_pre = None
 
     # ------------------------------------------------------------------ wiring
     def _layout(self, m_local: int, n_sh: int):
@@ -190,6 +195,11 @@ class P2PDecodeStep(StageEvents):
             p.ids_all[r] = reg.ids_all.data_ptr()
             p.w_all[r] = reg.w_all.data_ptr()
             p.flags[r] = reg.flags.data_ptr()
+        if self.fused:
+            p.epoch = self.epoch.data_ptr()
+            p.status = self.bar_status.data_ptr()
+            p.arrivals = self.arrivals.data_ptr()
+            p.timeout_ns = self.timeout_ns
         self.peers = p
         self.peer_regions = regions
 
@@ -207,6 +217,10 @@ class P2PDecodeStep(StageEvents):
             if r > 0:
                 s._ffn_pre = (lambda l, r=r: torch.cuda.current_stream().wait_event(evs[r - 1][l]))
             s._ffn_post = (lambda l, r=r: evs[r][l].record())
+            # one device: a combine grid spinning on the fused barrier must not hold the SMs the
+            # later ranks' persistent FFN grids need, so every combine also waits for every FFN
+            s._combine_pre = (lambda l: [torch.cuda.current_stream().wait_event(evs[q][l])
+                                         for q in range(len(steps))])
 
     def connect_ipc(self, group=None) -> None:
         """Multi-process: exchange CUDA IPC handles over `group` and map the peers' regions."""
@@ -248,7 +262,8 @@ class P2PDecodeStep(StageEvents):
             _lib.call("sere_route_topk_ep", ctypes.byref(self.peers), own_h.data_ptr(), layer.w_router_t.data_ptr(),
                       b.data_ptr() if b is not None else None, self.T_local, d_h, m.M, K,
                       self.route_ws.data_ptr(), self.route_ws.numel(), _moe._stream_ptr())
-            self._barrier()
+            if not self.fused:
+                self._barrier()
             if self._ffn_pre is not None:
                 self._ffn_pre(l)
             self._events_on(l)  # stages 0-3 inside sere_moe_ffn_ep, 4-5 around the combine
@@ -262,11 +277,14 @@ class P2PDecodeStep(StageEvents):
                       reg.h_all.data_ptr(), reg.ids_all.data_ptr(), reg.w_all.data_ptr(), self.T, K,
                       rr.new_indices.data_ptr(), rr.expert_class.data_ptr(), rr.reroute_map.data_ptr(),
                       rr.active_list.data_ptr(), rr.n_active.data_ptr(), reg.ws_ptr, ws_bytes,
-                      out.status.data_ptr(), _moe._stream_ptr())
+                      out.status.data_ptr(), ctypes.byref(self.peers) if self.fused else None, _moe._stream_ptr())
             dsim.validated = True
             if self._ffn_post is not None:
                 self._ffn_post(l)
-            self._barrier()
+            if not self.fused:
+                self._barrier()
+            elif self._combine_pre is not None:
+                self._combine_pre(l)
             _lib.call("sere_combine_ep", ctypes.byref(self.peers), rr.new_indices.data_ptr(), reg.ws_ptr,
                       self.hi - self.lo, bank.n_shared, self.n_shared_total, d_h, m.d_m, K, self.x.data_ptr(), None,
                       ctypes.c_float(self.eps), _moe._stream_ptr())
@@ -274,9 +292,10 @@ class P2PDecodeStep(StageEvents):
 
     @property
     def launches_per_step(self) -> int:
-        """Library kernels per step: router, 2 barriers, re-route/align, permute, fused FFN and
-        combine per layer, plus the first RMSNorm (the first layer's row copies not counted)."""
-        return self.model.L * 7 + 1
+        """Library kernels per step: router, re-route/align, permute, fused FFN and combine per
+        layer (+ 2 barrier kernels without the fused barriers), plus the first RMSNorm (the first
+        layer's row copies not counted)."""
+        return self.model.L * (5 if self.fused else 7) + 1
 
     def run(self) -> None:
         if self.graph is not None:

@@ -1,7 +1,13 @@
-# per-config layer benchmarks (BASELINE configs[1..3]) + the C4 headline, one JSON line each
+# per-config bench lines (BASELINE configs[1..3] + C4 variants), one full JSON line each, CPU baseline skipped
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for wl in c1 c2 c3; do
-  timeout 600 python bench.py --workload $wl --no-cpu-baseline --steps 50 --warmup 5 2>/dev/null | tail -1 >> gpurun_out/bench_configs.jsonl
+OUT=gpurun_out/r02_bench_configs.jsonl; rm -f $OUT
+run() { timeout 300 python bench.py --no-cpu-baseline --steps 30 --warmup 5 "$@" 2>/dev/null | tail -1 >> $OUT; }
+for sim in uniform clustered; do
+  for T in 64 128 256; do run --workload c1 --T $T --sim $sim; done
+  run --workload c3 --sim $sim
+  for S in 1 2; do for rho in 0 0.3 0.5 0.7 0.9 1.0; do run --workload c2 --retain $S --threshold $rho --sim $sim; done; done
 done
-timeout 600 python bench.py --workload c2 --beta 0 --no-cpu-baseline --steps 50 --warmup 5 2>/dev/null | tail -1 >> gpurun_out/bench_configs.jsonl
-timeout 600 python bench.py --workload c4 --sim clustered --no-cpu-baseline --steps 20 --warmup 3 2>/dev/null | tail -1 >> gpurun_out/bench_configs.jsonl
+run --workload c2 --beta 0
+run --workload c4 --sim clustered
+run --workload c4 --retain 2
+wc -l $OUT

@@ -161,6 +161,8 @@ def test_ep_peers_host_wiring():
     st.model = types.SimpleNamespace(M=M, K=K, d_h=d_h, d_m=d_m)
     st.world, st.rank, st.T, st.n_shared_total = world, 1, T, n_sh
     st.t0 = 16
+    st.fused = True
+    st.epoch, st.bar_status, st.arrivals, st.timeout_ns = _T(0x5000), _T(0x5100), _T(0x5200), 123456789
     regions = [types.SimpleNamespace(ws_ptr=(r + 1) << 32, h_all=_T(0x1000 + r), ids_all=_T(0x2000 + r),
                                      w_all=_T(0x3000 + r), flags=_T(0x4000 + r)) for r in range(world)]
     st._build_peers(regions)
@@ -175,3 +177,5 @@ def test_ep_peers_host_wiring():
         assert p.y_perm[r] == regions[r].ws_ptr + L.off_y_perm
         assert p.slot_row[r] == regions[r].ws_ptr + L.off_slot_row
         assert (p.h_all[r], p.ids_all[r], p.w_all[r], p.flags[r]) == (0x1000 + r, 0x2000 + r, 0x3000 + r, 0x4000 + r)
+    # this rank's fused-barrier state (include/sere_b200.h sere_ep_peers tail)
+    assert (p.epoch, p.status, p.arrivals, p.timeout_ns) == (0x5000, 0x5100, 0x5200, 123456789)

@@ -26,9 +26,14 @@ def _run(steps, streams):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,n_shared,mode,shape", [(2, 0, "sere", "small"), (4, 2, "sere", "small"),
-                                                       (2, 1, "topk", "small"), (2, 0, "sere", "c4")])
-def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shared, mode, shape):
+@pytest.mark.parametrize("world,n_shared,mode,shape,fused", [(2, 0, "sere", "small", True),
+                                                             (4, 2, "sere", "small", True),
+                                                             (2, 1, "topk", "small", True),
+                                                             (2, 0, "sere", "c4", True),
+                                                             (4, 2, "sere", "small", False)])
+def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shared, mode, shape, fused):
+    """fused: the barriers live in the router / FFN (arrive) and align / combine (wait) kernels;
+    otherwise two sere_ep_barrier kernels per layer."""
     import torch
 
     from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
@@ -39,8 +44,8 @@ def test_p2p_virtual_ranks_bit_exact_with_decode_step(cuda_device, world, n_shar
     else:
         L, M, K, d_h, d_m, T = 3, 32, 4, 512, 256, 64
     ref = DecodeStep(DecodeModel(L, M, K, d_h, d_m, n_shared=n_shared, seed=4, beta=1.0), T, 1, 0.5, mode)
-    steps = [P2PDecodeStep(m, T, world, r, 1, 0.5, mode) for r, m in enumerate(_shards(L, M, K, d_h, d_m,
-                                                                                        n_shared, world))]
+    steps = [P2PDecodeStep(m, T, world, r, 1, 0.5, mode, fused_barriers=fused)
+             for r, m in enumerate(_shards(L, M, K, d_h, d_m, n_shared, world))]
     P2PDecodeStep.connect_local(steps)
     streams = [torch.cuda.Stream() for _ in steps]
     try:
