@@ -405,23 +405,16 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
     }
   } else {  // unit prefixes over the schedule order
-    // a small active set (e.g. Qwen3 T=128 after SERE: 30 groups x 3 two-block units = 90 < 148
-    // SMs) would leave SMs idle for the whole gate/up phase: then every gate/up unit takes one
-    // 128-feature block (twice the units; the activation tile is re-read twice as often, which
-    // is cheap exactly when groups are small)
-    int tot_gu = 0;
-    for (int i = lane; i < G; i += 32) tot_gu += s_ugu[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) tot_gu += __shfl_xor_sync(0xffffffffu, tot_gu, off);
-    const int cap_gu = tot_gu < p.ffn_ctas ? 1 : kMwGuMax;
     int gu_base = 0, dn_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
       int ugu = 0, udn = 0;
       if (i < G) {
-        ugu = cap_gu == kMwGuMax ? s_ugu[i] : group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, cap_gu);
+        ugu = s_ugu[i];
         udn = s_udn[i];
-        plan[po.mw_gu + i] = cap_gu;
+        // (one-block gate/up units when the active set leaves SMs idle, e.g. Qwen3 T=128 after
+        // SERE with 90 two-block units for 148 SMs, measured slower: 0.626 vs 0.664 of peak)
+        plan[po.mw_gu + i] = kMwGuMax;
       }
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {

@@ -170,6 +170,7 @@ class P2PDecodeStep(StageEvents):
         self._ffn_pre = None
         self._ffn_post = None
         self._combine_pre = None
+        self._router_post = None
 
     # ------------------------------------------------------------------ wiring
     def _layout(self, m_local: int, n_sh: int):
@@ -213,9 +214,22 @@ class P2PDecodeStep(StageEvents):
         for s in steps:
             s._build_peers(regions)
         evs = [[torch.cuda.Event() for _ in range(s.model.L)] for s in steps]
+        rev = [[torch.cuda.Event() for _ in range(s.model.L)] for s in steps]
         for r, s in enumerate(steps):
-            if r > 0:
-                s._ffn_pre = (lambda l, r=r: torch.cuda.current_stream().wait_event(evs[r - 1][l]))
+            # one device: a kernel spinning on a fused barrier (the align kernel, launched early by
+            # PDL with the FFN grid queued behind it) must not hold the SMs another rank's router
+            # needs, so every rank's FFN stage also waits for every rank's router
+            s._router_post = (lambda l, r=r: rev[r][l].record())
+
+            def ffn_pre(l, r=r):
+                cur = torch.cuda.current_stream()
+                if r > 0:
+                    cur.wait_event(evs[r - 1][l])
+                if steps[r].fused:
+                    for q in range(len(steps)):
+                        cur.wait_event(rev[q][l])
+
+            s._ffn_pre = ffn_pre
             s._ffn_post = (lambda l, r=r: evs[r][l].record())
             # one device: a combine grid spinning on the fused barrier must not hold the SMs the
             # later ranks' persistent FFN grids need, so every combine also waits for every FFN
@@ -262,6 +276,8 @@ class P2PDecodeStep(StageEvents):
             _lib.call("sere_route_topk_ep", ctypes.byref(self.peers), own_h.data_ptr(), layer.w_router_t.data_ptr(),
                       b.data_ptr() if b is not None else None, self.T_local, d_h, m.M, K,
                       self.route_ws.data_ptr(), self.route_ws.numel(), _moe._stream_ptr())
+            if self._router_post is not None:
+                self._router_post(l)
             if not self.fused:
                 self._barrier()
             if self._ffn_pre is not None:
