@@ -259,6 +259,13 @@ class P2PDecodeStep(StageEvents):
                   ctypes.c_int64(self.timeout_ns), _moe._stream_ptr())
 
     def _launch(self) -> None:
+        for _ in self._phases():
+            pass
+
+    def _phases(self):
+        """The step's launches, yielding after each phase (prologue; then per layer router,
+        FFN stage, combine) so that virtual ranks sharing one device can be interleaved phase
+        by phase (`run_local`): every cross-rank event is recorded before it is waited on."""
         if self.peers is None:
             raise RuntimeError("P2PDecodeStep is not connected (connect_local / connect_ipc)")
         m, reg = self.model, self.region
@@ -270,6 +277,7 @@ class P2PDecodeStep(StageEvents):
         for r, peer in enumerate(self.peer_regions):  # first layer's input rows to every rank
             if r != self.rank:
                 peer.h_all[self.t0:self.t1].copy_(own_h)
+        yield
         ws_bytes = reg.ws_bytes
         for l, layer in enumerate(m.layers):
             b = layer.bias
@@ -280,6 +288,7 @@ class P2PDecodeStep(StageEvents):
                 self._router_post(l)
             if not self.fused:
                 self._barrier()
+            yield
             if self._ffn_pre is not None:
                 self._ffn_pre(l)
             self._events_on(l)  # stages 0-3 inside sere_moe_ffn_ep, 4-5 around the combine
@@ -299,12 +308,29 @@ class P2PDecodeStep(StageEvents):
                 self._ffn_post(l)
             if not self.fused:
                 self._barrier()
-            elif self._combine_pre is not None:
+            yield
+            if self.fused and self._combine_pre is not None:
                 self._combine_pre(l)
             _lib.call("sere_combine_ep", ctypes.byref(self.peers), rr.new_indices.data_ptr(), reg.ws_ptr,
                       self.hi - self.lo, bank.n_shared, self.n_shared_total, d_h, m.d_m, K, self.x.data_ptr(), None,
                       ctypes.c_float(self.eps), _moe._stream_ptr())
             self._events_off()
+            yield
+
+    @staticmethod
+    def run_local(steps: list, streams: list) -> None:
+        """One eager step of virtual ranks on one device (connect_local), each on its own
+        stream, launched phase by phase in rank order."""
+        torch = _torch()
+        gens = [st._phases() for st in steps]
+        live = list(range(len(steps)))
+        while live:
+            for r in list(live):
+                with torch.cuda.stream(streams[r]):
+                    try:
+                        next(gens[r])
+                    except StopIteration:
+                        live.remove(r)
 
     @property
     def launches_per_step(self) -> int:

@@ -169,9 +169,7 @@ def test_p2p_two_ranks_block_vs_fp64_oracle(cuda_device):
         for st in steps:
             st.x_in.copy_(x0[st.t0:st.t1])
         torch.cuda.synchronize()
-        for st, s in zip(steps, streams):
-            with torch.cuda.stream(s):
-                st.run()
+        P2PDecodeStep.run_local(steps, streams)
         torch.cuda.synchronize()
         for st in steps:
             st.check()

@@ -17,9 +17,9 @@ def _shards(L, M, K, d_h, d_m, n_shared, world):
 def _run(steps, streams):
     import torch
 
-    for st, s in zip(steps, streams):
-        with torch.cuda.stream(s):
-            st.run()
+    from paper_2602_07616_b200.ep_p2p import P2PDecodeStep
+
+    P2PDecodeStep.run_local(steps, streams)
     torch.cuda.synchronize()
     for st in steps:
         st.check()
