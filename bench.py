@@ -448,7 +448,13 @@ def run_ours(args, wl):
     topk.check()
 
     clocks.start()
+    if hasattr(sere, "wait_ns"):
+        sere.wait_ns.zero_()
     ms_sere = time_region(torch, sere.run, args.steps, world)
+    wait_us = None
+    if hasattr(sere, "wait_ns") and getattr(sere, "fused", False):  # fused-barrier waits of this rank
+        w = sere.wait_ns.double().cpu().numpy() / 1e3 / (args.steps * L)
+        wait_us = {"align_side_us_per_layer": round(float(w[0]), 2), "combine_side_us_per_layer": round(float(w[1]), 2)}
     ms_topk = time_region(torch, topk.run, args.steps, world)
     # end-to-end through the public call: pinned host x -> step -> pinned host result
     x_host = x_local.cpu().pin_memory()
@@ -591,6 +597,21 @@ def run_ours(args, wl):
         except MemoryError as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "port", "sample": f"skipped: {exc}"}
 
+    ep_info = None
+    if world > 1:  # per-rank collective (barrier) time share and FFN roofline, gathered to rank 0
+        import torch.distributed as dist
+
+        mine = {"rank": rank, "experts": [lo, hi], "barrier_wait": wait_us,
+                "barrier_share_of_step": (round((wait_us["align_side_us_per_layer"] + wait_us["combine_side_us_per_layer"])
+                                                * L / (ms_sere * 1e3), 4) if wait_us else None),
+                "ffn_frac_in_step": sp_sere["ffn_frac"] if sp_sere else None,
+                "ffn_us_per_layer": sp_sere["ffn_us_per_layer_avg"] if sp_sere else None,
+                "stage_us_per_layer": sp_sere["stage_us_per_layer_avg"] if sp_sere else None}
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        ep_info = {"transport": transport, "ranks": allr,
+                   "note": "barrier_wait: device time the re-route/align kernel and the combine spent in the fused "
+                           "peer-memory barriers (timed region, per layer); stages: CUDA events per stage"}
     tok_s = T / (ms_sere * 1e-3)
     tok_s_topk = T / (ms_topk * 1e-3)
     line = {
@@ -620,6 +641,7 @@ def run_ours(args, wl):
         "roofline": roof,
         "cpu_baseline": cpu,
         "ep_transport": transport,
+        "ep": ep_info,
         "cuda_graph": all(graphed),
         "e2e": {"value": round(T / (ms_e2e * 1e-3), 1), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4),

@@ -265,6 +265,8 @@ typedef struct {
   int32_t* status;   /* device status word: SERE_ERR_CUDA after a timeout / abort           */
   int32_t* arrivals; /* device counter of router CTAs (zeroed once)                          */
   int64_t timeout_ns;
+  uint64_t* wait_ns; /* optional device [2]: ns spent waiting in the fused barriers, added by
+                        the re-route/align kernel [0] and the combine [1] (NULL: not measured) */
 } sere_ep_peers;
 
 /* Router for this rank's T_local = T_all/world tokens (x_local = own h_all rows

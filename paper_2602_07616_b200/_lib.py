@@ -42,6 +42,7 @@ class EpPeers(ctypes.Structure):
         ("status", ctypes.c_void_p),
         ("arrivals", ctypes.c_void_p),
         ("timeout_ns", ctypes.c_int64),
+        ("wait_ns", ctypes.c_void_p),
     ]
 
 

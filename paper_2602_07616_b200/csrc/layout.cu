@@ -300,7 +300,11 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
     pdl_wait();  // peers' slot rows are ordered by the barrier kernel before us: wait for it
     if (ep.epoch != nullptr) {  // fused barrier: every rank's expert outputs are final
       __shared__ int s_ok;
-      if (threadIdx.x == 0) s_ok = ep_wait(ep_sync_dev(ep));
+      if (threadIdx.x == 0) {
+        EpSync sy = ep_sync_dev(ep);
+        if (blockIdx.x != 0) sy.wait_ns = nullptr;  // CTA 0 stands for the pass
+        s_ok = ep_wait(sy);
+      }
       __syncthreads();
       if (!s_ok) return;
     }

@@ -23,6 +23,8 @@ struct EpSync {
   int32_t* epoch;               // this rank's epoch counter
   int32_t* status;              // this rank's barrier status word (SERE_ERR_CUDA on timeout / abort)
   long long timeout_ns;
+  unsigned long long* wait_ns;  // optional: accumulated wait time [0] align side, [1] combine side
+  int wait_slot;
 };
 
 struct AlignParams {
@@ -125,6 +127,7 @@ struct EpPeers {
   int32_t* status;
   int32_t* arrivals;                  // router CTAs done (the last one arrives)
   long long timeout_ns;
+  unsigned long long* wait_ns;        // optional barrier wait accumulators (see EpSync)
 };
 
 // flags[r] holds kMaxEpRanks barrier slots followed by rank r's sticky ABORT word: a
@@ -152,6 +155,8 @@ __host__ __device__ inline EpSync ep_sync_dev(const EpPeers& ep) {
   s.epoch = ep.epoch;
   s.status = ep.status;
   s.timeout_ns = ep.timeout_ns;
+  s.wait_ns = ep.wait_ns;
+  s.wait_slot = 1;  // the combine side
   return s;
 }
 inline EpSync ep_sync_of(const EpPeers& ep) {
@@ -163,6 +168,8 @@ inline EpSync ep_sync_of(const EpPeers& ep) {
   s.epoch = ep.epoch;
   s.status = ep.status;
   s.timeout_ns = ep.timeout_ns;
+  s.wait_ns = ep.wait_ns;
+  s.wait_slot = 0;  // the align side
   return s;
 }
 // one thread: this rank's writes so far (made system-visible by the caller's fences) are
@@ -193,6 +200,11 @@ __device__ __forceinline__ bool ep_wait(const EpSync& s) {
         return false;
       }
     }
+  }
+  if (s.wait_ns) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicAdd(s.wait_ns + s.wait_slot, t - t0);
   }
   __threadfence();
   return true;

@@ -147,6 +147,7 @@ class P2PDecodeStep(StageEvents):
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)
         self.bar_status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.arrivals = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.wait_ns = torch.zeros(2, dtype=torch.int64, device=dev)  # fused-barrier waits: align, combine
         # fused barriers: the router's last CTA and the FFN's last CTA arrive, the align kernel and
         # the combine wait (5 launches per layer); False: two sere_ep_barrier kernels (7 launches)
         self.fused = bool(fused_barriers)
@@ -201,6 +202,7 @@ class P2PDecodeStep(StageEvents):
             p.status = self.bar_status.data_ptr()
             p.arrivals = self.arrivals.data_ptr()
             p.timeout_ns = self.timeout_ns
+            p.wait_ns = self.wait_ns.data_ptr()
         self.peers = p
         self.peer_regions = regions
 

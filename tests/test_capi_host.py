@@ -163,6 +163,7 @@ def test_ep_peers_host_wiring():
     st.t0 = 16
     st.fused = True
     st.epoch, st.bar_status, st.arrivals, st.timeout_ns = _T(0x5000), _T(0x5100), _T(0x5200), 123456789
+    st.wait_ns = _T(0x5300)
     regions = [types.SimpleNamespace(ws_ptr=(r + 1) << 32, h_all=_T(0x1000 + r), ids_all=_T(0x2000 + r),
                                      w_all=_T(0x3000 + r), flags=_T(0x4000 + r)) for r in range(world)]
     st._build_peers(regions)
@@ -178,4 +179,4 @@ def test_ep_peers_host_wiring():
         assert p.slot_row[r] == regions[r].ws_ptr + L.off_slot_row
         assert (p.h_all[r], p.ids_all[r], p.w_all[r], p.flags[r]) == (0x1000 + r, 0x2000 + r, 0x3000 + r, 0x4000 + r)
     # this rank's fused-barrier state (include/sere_b200.h sere_ep_peers tail)
-    assert (p.epoch, p.status, p.arrivals, p.timeout_ns) == (0x5000, 0x5100, 0x5200, 123456789)
+    assert (p.epoch, p.status, p.arrivals, p.timeout_ns, p.wait_ns) == (0x5000, 0x5100, 0x5200, 123456789, 0x5300)
