@@ -224,7 +224,7 @@ def time_region(torch, fn, steps, world, sync_group=None):
         dist.barrier()
     ms = s.elapsed_time(e) / steps
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return ms
@@ -363,11 +363,18 @@ def run_ours(args, wl):
     world, rank, local = dist_env()
     if args.gpus > 1 and world == 1:
         raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    # SERE_BENCH_DEVICE: put every rank on one device (a smoke run of the N>1 path on a 1-GPU box;
+    # ranks time-slice the device, so its numbers are not a measurement)
+    dev_override = os.environ.get("SERE_BENCH_DEVICE")
+    local = int(dev_override) if dev_override is not None else local
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dev_override is not None:  # several ranks on one device: NCCL refuses that, gloo does not
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2602_07616_b200 import build as _build
 
     if rank == 0:
@@ -432,7 +439,7 @@ def run_ours(args, wl):
     if transport == "p2p":  # every rank takes the same transport
         import torch.distributed as dist
 
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
             print(f"[bench] peer-memory EP unavailable ({err}); using NCCL collectives", file=sys.stderr)
