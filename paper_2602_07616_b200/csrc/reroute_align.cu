@@ -405,6 +405,22 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
     }
   } else {  // unit prefixes over the schedule order
+    // A small active set leaves SMs idle for the whole gate/up phase (Qwen3 T=128 after SERE:
+    // 31 groups x 3 two-block units = 93 units for 148 SMs, every group's h complete only at
+    // the end of it). Then the first groups in schedule order (the largest) take one-block
+    // gate/up units while the total still fits one wave: they finish in half the time, and
+    // their down units (first in the down order) fill the SMs that free up.
+    if (lane == 0) {
+      int tot = 0;
+      for (int i = 0; i < G; ++i) tot += s_ugu[i];
+      for (int i = 0; i < G && tot < p.ffn_ctas; ++i) {
+        const int u1 = group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, 1);
+        if (tot + u1 - s_ugu[i] > p.ffn_ctas) break;
+        tot += u1 - s_ugu[i];
+        s_ugu[i] = -u1;  // negative: one-block units
+      }
+    }
+    __syncwarp();
     int gu_base = 0, dn_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
@@ -412,9 +428,8 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       if (i < G) {
         ugu = s_ugu[i];
         udn = s_udn[i];
-        // (one-block gate/up units when the active set leaves SMs idle, e.g. Qwen3 T=128 after
-        // SERE with 90 two-block units for 148 SMs, measured slower: 0.626 vs 0.664 of peak)
-        plan[po.mw_gu + i] = kMwGuMax;
+        plan[po.mw_gu + i] = ugu < 0 ? 1 : kMwGuMax;
+        ugu = ugu < 0 ? -ugu : ugu;
       }
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {
