@@ -17,7 +17,8 @@
 //  * weights live in the bank as contiguous 16 KB pre-swizzled tiles (one bulk async
 //    copy each, TMA engine); activations come from the grouped swizzled buffers
 //    (L2-resident, evict-last);
-//  * shared memory is a ring of 13 x 16 KB pages; a pipeline step covers kKT k-tiles (1):
+//  * shared memory is a ring of 13 x 16 KB = 104 granules of 2 KB (an activation tile of
+//    n_mma rows takes n_mma/16 granules, a weight tile 8); a pipeline step covers kKT k-tiles (1):
 //    their B tiles and the unit's A tiles, consecutive pages, one (full, empty) mbarrier
 //    pair from an 8-entry ring and one commit, so the stream never drains across unit
 //    boundaries;
@@ -53,7 +54,16 @@ namespace sere {
 
 constexpr int kPages = 13;
 constexpr int kPageBytes = 16384;
-constexpr int kEntries = 8;   // k-step barrier ring
+// The operand ring is allocated in 2 KB granules: a weight tile takes 8, an activation tile
+// n_mma/16 (a 16-row down tile 1 instead of a whole 16 KB page), so small-N k-steps keep more
+// weight bytes in flight per SM
+constexpr int kGranBytes = 2048;
+constexpr int kGrans = kPages * kPageBytes / kGranBytes;
+constexpr int kTileGrans = kPageBytes / kGranBytes;
+#ifndef SERE_KENTRIES
+#define SERE_KENTRIES 12
+#endif
+constexpr int kEntries = SERE_KENTRIES;   // k-step barrier ring
 constexpr int kQueue = 4;     // unit-id queue producer -> MMA / epilogue
 constexpr int kTq = 4;        // TMEM unit slots (barrier pairs)
 #ifndef SERE_EPI_WARPS
@@ -153,10 +163,12 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_groups, int units_gu, c
 constexpr int kKT = SERE_KT;  // 64-wide k-tiles per pipeline step (1: finest-grained page release; 2 measured slower)
 // A tiles (= TMEM accumulators) of one k-tile: gate and up per gate/up feature block, one per down m-tile
 __device__ __forceinline__ int kstep_atiles(const Unit& U) { return U.dn ? U.mwu : 2 * U.mwu; }
-// pages of the B tile of one k-tile (1 up to 128 rows, 2 up to 256)
-__device__ __forceinline__ int ktile_bpages(const Unit& U) { return U.n_mma > 128 ? 2 : 1; }
-// pages of a step of nk k-tiles: the nk B tiles, then per m-tile block j its nk k-tiles' A tiles
-__device__ __forceinline__ int kstep_pages(const Unit& U, int nk) { return nk * (ktile_bpages(U) + kstep_atiles(U)); }
+// granules of the B tile of one k-tile (n_mma rows of 128 B)
+__device__ __forceinline__ int ktile_bgrans(const Unit& U) { return U.n_mma / 16; }
+// granules of a step of nk k-tiles: the nk B tiles, then per m-tile block j its nk k-tiles' A tiles
+__device__ __forceinline__ int kstep_grans(const Unit& U, int nk) {
+  return nk * (ktile_bgrans(U) + kstep_atiles(U) * kTileGrans);
+}
 
 __device__ __forceinline__ bool ranges_overlap(int a, int na, int b, int nb) { return a < b + nb && b < a + na; }
 
@@ -316,13 +328,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
                   (static_cast<unsigned long long>(U.n_mma) << 44) | (static_cast<unsigned long long>(U.dn) << 53);
           ut[2] = globaltimer_ns();
         }
-        const int bpk = ktile_bpages(U);
+        const int bgr = ktile_bgrans(U);
         const uint32_t b_bytes = static_cast<uint32_t>(U.n_mma) * 128u;
         for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
           const int nk = min(kKT, U.kt_end - kt);
-          const int np = kstep_pages(U, nk), bp = nk * bpk;
+          const int np = kstep_grans(U, nk);
+          const size_t a_off = static_cast<size_t>(nk) * bgr * kGranBytes;  // A tiles follow the nk B tiles
           const uint32_t tx = nk * (b_bytes + ((p.dbg_mode & 1) ? 0u : static_cast<uint32_t>(U.mwu) * a_copy));
-          if (head + np > kPages) head = 0;
+          if (head + np > kGrans) head = 0;
           // release in FIFO order until this k-step's entry and pages are free of every
           // in-flight k-step (after a wrap the overlap can be with the youngest ones)
           for (;;) {
@@ -339,26 +352,26 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int e = kstep % kEntries;
           tail->e_page[e] = head;
           tail->e_np[e] = np;
-          uint8_t* pg = smem + head * kPageBytes;
+          uint8_t* pg = smem + static_cast<size_t>(head) * kGranBytes;
           mbar_arrive_expect_tx(&tail->full[e], tx);
           if (!(p.dbg_mode & 1)) {
             if (U.dn) {  // k-tile kk: the unit's 1-2 adjacent m-tiles, one copy (pages kk-major)
               for (int kk = 0; kk < nk; ++kk) {
-                bulk_g2s(pg + (bp + kk * U.mwu) * kPageBytes,
+                bulk_g2s(pg + a_off + static_cast<size_t>(kk * U.mwu) * kPageBytes,
                          a_unit + static_cast<size_t>(kt + kk) * kW2Group * kTileBytes, U.mwu * kTileBytes,
                          &tail->full[e], pol_w);
               }
             } else {  // feature block j at k-tiles kt..kt+nk-1: gate/up tiles, one contiguous copy
               const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
               for (int j = 0; j < U.mwu; ++j)
-                bulk_g2s(pg + bp * kPageBytes + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy,
+                bulk_g2s(pg + a_off + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy,
                          &tail->full[e], pol_w);
             }
           }
           const bool gated = !pdl_done || dep_g >= 0;
           if (gated && n_pend + nk > kPdlPrefetch) pdl_flush();
           for (int kk = 0; kk < nk; ++kk) {
-            uint8_t* bdst = pg + kk * bpk * kPageBytes;
+            uint8_t* bdst = pg + static_cast<size_t>(kk * bgr) * kGranBytes;
             const uint8_t* bsrc = b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128;
             if (pdl_done && dep_g < 0) {
               bulk_g2s(bdst, bsrc, b_bytes, &tail->full[e], pol_x);
@@ -418,27 +431,28 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         tail->t_col[mi][iter % kTq] = col;
         tail->t_need[mi][iter % kTq] = need;
         tc_fence_after();
-        const int bpk = ktile_bpages(U), apj = U.dn ? 1 : 2;  // A tiles per m-tile block and k-tile
+        const int bgr = ktile_bgrans(U), apj = U.dn ? 1 : 2;  // A tiles per m-tile block and k-tile
         const uint32_t idesc = umma_idesc_bf16(128, U.n_mma);
         const uint32_t d0 = tmem_base + col;
         for (int kt = U.kt_begin; kt < U.kt_end; kt += kKT, ++kstep) {
           const int nk = min(kKT, U.kt_end - kt);
-          const int np = kstep_pages(U, nk), bp = nk * bpk;
-          if (head + np > kPages) head = 0;
+          const int np = kstep_grans(U, nk);
+          const uint32_t a_off = static_cast<uint32_t>(nk * bgr * kGranBytes);
+          if (head + np > kGrans) head = 0;
           const int e = kstep % kEntries;
           mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u,
                           acc_full ? (U.dn ? &w_full_dn : acc_full) : nullptr);
           nks_dn += U.dn;
           tc_fence_after();
-          const uint32_t pg_addr = smem_u32(smem + head * kPageBytes);
+          const uint32_t pg_addr = smem_u32(smem + static_cast<size_t>(head) * kGranBytes);
           if (!(p.dbg_mode & 2)) {
             for (int kk = 0; kk < nk; ++kk) {
-              const uint32_t b_addr = pg_addr + kk * bpk * kPageBytes;
+              const uint32_t b_addr = pg_addr + kk * bgr * kGranBytes;
               for (int j = 0; j < U.mwu; ++j) {
                 for (int s2 = 0; s2 < apj; ++s2) {  // accumulator j*apj + s2 (gate/up: gate then up)
                   if ((j * apj + s2) % kMmaWarps != mi) continue;
-                  const int apage = U.dn ? bp + kk * U.mwu + j : bp + (j * nk + kk) * apj + s2;
-                  const uint32_t a_addr = pg_addr + apage * kPageBytes;
+                  const int apage = U.dn ? kk * U.mwu + j : (j * nk + kk) * apj + s2;
+                  const uint32_t a_addr = pg_addr + a_off + apage * kPageBytes;
                   const uint32_t dj = d0 + (j * apj + s2) * U.n_mma;
 #pragma unroll
                   for (int k = 0; k < 4; ++k) {
