@@ -1,9 +1,9 @@
 """Summaries for profiles/ from a gpu_round.sh capture (run here, on the copied-back files).
 
-    python scripts/ncu_summarize.py TAG [--rep gpurun_out/prof_ffn.ncu-rep] [--launches gpurun_out/launches.csv]
+    python scripts/ncu_summarize.py TAG [--round r02] [--rep gpurun_out/prof_ffn.ncu-rep] [--launches gpurun_out/launches.csv]
 
-Writes profiles/r01_ncu_summary_TAG.txt, profiles/r01_ncu_traffic_TAG.json (per-launch DRAM
-bytes of moe_ffn_kernel next to its algorithmic bytes) and profiles/r01_launches_TAG.csv /
+Writes profiles/RR_ncu_summary_TAG.txt, profiles/RR_ncu_traffic_TAG.json (per-launch DRAM
+bytes of moe_ffn_kernel next to its algorithmic bytes) and profiles/RR_launches_TAG.csv /
 _summary.txt (the serialised launch list's per-kernel share)."""
 import argparse
 import csv
@@ -19,7 +19,16 @@ METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.
            "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active", "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum",
            "lts__t_sectors_srcunit_tex_op_read.sum", "smsp__cycles_active.avg", "gpc__cycles_elapsed.max",
-           "launch__grid_size", "launch__block_size", "launch__registers_per_thread"]
+           "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+           # tensor pipe (tcgen05 UTCHMMA) utilisation of the grouped GEMM
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum",
+           "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "smsp__mem_tensor_writes_op_utcmma.sum", "smsp__sass_inst_executed_op_tmem_ldt.sum",
+           "dram__bytes_read.sum.pct_of_peak_sustained_elapsed"]
 D_H, D_M = 2048, 768
 
 
@@ -43,9 +52,10 @@ def main():
     ap.add_argument("--rep", default="gpurun_out/prof_ffn.ncu-rep")
     ap.add_argument("--launches", default="gpurun_out/launches.csv")
     ap.add_argument("--note", default="")
+    ap.add_argument("--round", default="r02")
     a = ap.parse_args()
     rows, units = raw(a.rep)
-    lines = [f"# r01 ncu summary {a.tag}: ncu --set full --clock-control none --import-source on; "
+    lines = [f"# {a.round} ncu summary {a.tag}: ncu --set full --clock-control none --import-source on; "
              f"profile_step --layers 2 (C4, SERE S=1 rho=0.5 beta=1). {a.note}"]
     launches = []
     for i, r in enumerate(rows):
@@ -72,10 +82,10 @@ def main():
         if i < len(actives):
             L["active_experts"] = actives[i]
             L["algorithmic_bytes"] = 2 * 3 * D_H * D_M * actives[i] + 2 * 512 * D_H + 4 * 512 * D_H + 8 * 512 * 8
-    (ROOT / f"profiles/r01_ncu_summary_{a.tag}.txt").write_text("\n".join(lines) + "\n")
+    (ROOT / f"profiles/{a.round}_ncu_summary_{a.tag}.txt").write_text("\n".join(lines) + "\n")
     if launches and all("algorithmic_bytes" in L for L in launches):
-        (ROOT / f"profiles/r01_ncu_traffic_{a.tag}.json").write_text(json.dumps(
-            {"kernel": "moe_ffn_kernel", "source": f"profiles/r01_ncu_summary_{a.tag}.txt", "launches": launches,
+        (ROOT / f"profiles/{a.round}_ncu_traffic_{a.tag}.json").write_text(json.dumps(
+            {"kernel": "moe_ffn_kernel", "source": f"profiles/{a.round}_ncu_summary_{a.tag}.txt", "launches": launches,
              "note": "ncu flushes L2 before each replay, so activation/h reads that are L2 hits in the graph-replayed "
                      "step count as DRAM here"}, indent=1) + "\n")
     print("\n".join(lines))
@@ -96,8 +106,8 @@ def main():
             for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
                 out.append(f"{k:32s} launches={len(v):3d} avg_us={sum(v)/len(v):8.2f} share={sum(v)/tot:.3f}")
             out.append(f"total us {tot:.1f}")
-            (ROOT / f"profiles/r01_launches_{a.tag}_summary.txt").write_text("\n".join(out) + "\n")
-            (ROOT / f"profiles/r01_launches_{a.tag}.csv").write_text(txt)
+            (ROOT / f"profiles/{a.round}_launches_{a.tag}_summary.txt").write_text("\n".join(out) + "\n")
+            (ROOT / f"profiles/{a.round}_launches_{a.tag}.csv").write_text(txt)
             print("\n".join(out))
 
 
