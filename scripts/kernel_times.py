@@ -16,7 +16,7 @@ def main():
     ap.add_argument("--mode", default="sere")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--T", type=int, default=512)
-    ap.add_argument("--pdl", type=int, default=0)
+    ap.add_argument("--pdl", type=int, default=-1, help="sere_set_pdl mask (-1: library default)")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -26,7 +26,8 @@ def main():
 
     build.build()
     from paper_2602_07616_b200 import _lib
-    _lib.load().sere_set_pdl(a.pdl)
+    if a.pdl >= 0:
+        _lib.load().sere_set_pdl(a.pdl)
     model = DecodeModel(a.layers, 128, 8, 2048, 768, seed=0, beta=1.0)
     step = DecodeStep(model, a.T, 1, 0.5, a.mode)
     step.set_input(torch.randn(a.T, 2048, device="cuda"))
@@ -51,6 +52,14 @@ def main():
     starts = sorted((e.time_range.start, e.time_range.end) for e in evs)
     span = (starts[-1][1] - starts[0][0]) / a.steps
     print(f"  wall span per step {span / 1e3:.3f} ms (gaps+launch {(span - per_step) / a.layers:.1f} us/layer)")
+    # chain view: for each kernel, start minus the previous kernel's end (negative = PDL overlap)
+    seq = sorted(((e.time_range.start, e.time_range.end, e.name.split("(")[0]) for e in evs))
+    gap = defaultdict(list)
+    for (s0, e0, n0), (s1, e1, n1) in zip(seq, seq[1:]):
+        gap[n1].append(s1 - e0)
+    for n, v in sorted(gap.items(), key=lambda kv: -len(kv[1])):
+        v = sorted(v)
+        print(f"  gap before {n[:40]:40s} n={len(v):5d} avg {sum(v) / len(v):7.2f} us  median {v[len(v) // 2]:7.2f} us")
 
 
 if __name__ == "__main__":
