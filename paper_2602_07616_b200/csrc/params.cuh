@@ -51,6 +51,7 @@ struct AlignParams {
   int32_t* ids_final;     // [T,K] the (re-routed) table the layer runs on (align mode; the permute reads it)
   uint16_t* blk_prefix;   // [TB][Et] cells of bank expert e in token blocks before tb (align mode)
   EpSync sync;            // expert parallel: wait for every rank's router rows before reading the table
+  int stage_sim;          // set by launch_reroute_align: the sim is bulk-copied into shared memory
 };
 
 struct FfnParams {

@@ -36,13 +36,19 @@ __host__ __device__ inline size_t align_smem_bytes(int T, int K, int M, int Et) 
   const int TK = T * K, TB = (T + kTokBlk - 1) / kTokBlk;
   size_t b = 0;
   b += static_cast<size_t>(TK) * 4;                   // s_ids
-  b += static_cast<size_t>(M) * 4 * 2;                // s_map, s_list
+  b += static_cast<size_t>(M) * 4;                    // s_map
   b += static_cast<size_t>(Et) * 4 * 4;               // s_cnt, s_row0, s_gpad, s_sched
   b += static_cast<size_t>(round_up(TB * Et, 2)) * 2; // s_cntb (u16 pairs updated by 32-bit atomics)
-  b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_need, s_cls
+  b += static_cast<size_t>(round_up(M, 4)) * 3;       // s_hflag, s_sec, s_cls
   return round_up(static_cast<int>(b), 16);
 }
-__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }
+// The similarity matrix is staged into shared memory after the fixed arrays when it fits: one
+// bulk copy issued BEFORE the PDL wait (the sim is static per layer, so the copy overlaps the
+// router); the argmax then reads shared memory instead of L2.
+constexpr size_t kAlignSmemCap = 200 * 1024;
+__host__ __device__ inline size_t align_smem_total(int T, int K, int M, int Et, bool stage_sim) {
+  return align_smem_bytes(T, K, M, Et) + (stage_sim ? static_cast<size_t>(M) * M * 8 : 0);
+}
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const int lane = lane_id();
@@ -61,16 +67,17 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   const int e_lo = p.e_lo, m_loc = p.m_local, Et = m_loc + p.n_shared;  // expert-parallel ownership
   int32_t* s_ids = reinterpret_cast<int32_t*>(smem);
   int32_t* s_map = s_ids + TK;
-  int32_t* s_list = s_map + M;   // compact list of needed secondaries
-  int32_t* s_cnt = s_list + M;   // per bank-expert totals
+  int32_t* s_cnt = s_map + M;    // per bank-expert totals
   int32_t* s_row0 = s_cnt + Et;  // first permuted row of each bank expert's group
   int32_t* s_gpad = s_row0 + Et;  // padded rows of group g
   int32_t* s_sched = s_gpad + Et; // schedule order of the groups
   uint16_t* s_cntb = reinterpret_cast<uint16_t*>(s_sched + Et);  // [TB][Et] counts -> prefixes
   uint8_t* s_hflag = reinterpret_cast<uint8_t*>(s_cntb + round_up(TB * Et, 2));
-  uint8_t* s_need = s_hflag + round_up(M, 4);
-  uint8_t* s_cls = s_need + round_up(M, 4);
-  __shared__ int s_err_id, s_err_sim, s_err_route, s_err_domain, s_nneed;
+  uint8_t* s_sec = s_hflag + round_up(M, 4);   // expert named by some slot >= S
+  uint8_t* s_cls = s_sec + round_up(M, 4);
+  const double* s_sim = reinterpret_cast<const double*>(smem + align_smem_bytes(T, K, M, Et));  // if p.stage_sim
+  __shared__ int s_err_id, s_err_sim, s_err_route, s_err_domain;
+  __shared__ __align__(8) uint64_t s_sim_bar;
 
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
@@ -79,8 +86,22 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   const int s_eff = S < K ? S : K;  // S == K: identity re-routing, every routed expert is primary
   auto local_of = [&](int e) { return (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1; };
 
-  if (tid == 0) { s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0; }
-  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_need[e] = 0; }
+  const bool stage = reroute && p.stage_sim;
+  if (tid == 0) {
+    s_err_id = 0; s_err_sim = 0; s_err_route = 0; s_err_domain = 0;
+    if (stage) {  // static data: issued before the PDL wait, lands while the router runs
+      mbar_init(&s_sim_bar, 1);
+      fence_mbar_init();
+      const uint32_t bytes = static_cast<uint32_t>(M) * M * 8;
+      mbar_arrive_expect_tx(&s_sim_bar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(s_sim)),
+          "l"(p.sim), "r"(bytes), "r"(smem_u32(&s_sim_bar))
+          : "memory");
+    }
+  }
+  for (int e = tid; e < M; e += nthr) { s_map[e] = -1; s_cls[e] = 0; s_hflag[e] = 0; s_sec[e] = 0; }
   if (align)
     for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr) reinterpret_cast<uint32_t*>(s_cntb)[i] = 0u;
   __syncthreads();
@@ -90,6 +111,7 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
     if (tid == 0 && !ep_wait(p.sync)) s_err_domain = -1;
     __syncthreads();
     if (s_err_domain < 0) {
+      if (stage) mbar_wait(&s_sim_bar, 0);  // no CTA exit with the bulk copy in flight
       if (tid == 0) {
         if (p.status_dev) *p.status_dev = SERE_ERR_CUDA;
         if (p.plan) p.plan[P_STATUS] = SERE_ERR_CUDA;
@@ -119,14 +141,19 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         const bool ok = v >= 0 && v < M;
         bad |= !ok;
         if (v == SERE_ID_NONFINITE) s_err_domain = 1;  // the router saw a non-finite token state
-        if (reroute && ok && k < s_eff) s_hflag[v] = 1;  // primary set H (rerouting.py:147; Alg. 2 l.467-471)
+        if (reroute && ok) {
+          if (k < s_eff) s_hflag[v] = 1;  // primary set H (rerouting.py:147; Alg. 2 l.467-471)
+          else s_sec[v] = 1;              // a secondary candidate (needed unless primary, below)
+        }
       }
     }
     if (bad) s_err_id = 1;
   }
+  if (stage) mbar_wait(&s_sim_bar, 0);
+  const double* simr = stage ? s_sim : p.sim;
   if (reroute && (p.flags & SERE_FLAG_CHECK_SIM)) {  // rerouting.py:115-116 (NaN passes, as there)
     for (int i = tid; i < M * M; i += nthr) {
-      const double v = p.sim[i];
+      const double v = simr[i];
       if (v < 0.0 || v > 1.0) s_err_sim = 1;
     }
   }
@@ -143,50 +170,31 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   }
 
   if (reroute) {
-    // ---- distinct secondaries: experts of slots >= S that are not primary (rerouting.py:152-156)
-    if (S < K)
-      for (int t = tid; t < T; t += nthr)
-        for (int k = S; k < K; ++k) {
-          const int e = s_ids[k * T + t];
-          if (!s_hflag[e]) s_need[e] = 1;
-        }
-    __syncthreads();
-    SERE_PHASE(2);
-    if (warp == 0) {  // ascending compact list of the secondaries
-      int base = 0;
-      for (int c0 = 0; c0 < M; c0 += 32) {
-        const int e = c0 + lane;
-        const bool nd = e < M && s_need[e];
-        const unsigned m = __ballot_sync(0xffffffffu, nd);
-        if (nd) s_list[base + __popc(m & ((1u << lane) - 1u))] = e;
-        base += __popc(m);
-      }
-      if (lane == 0) s_nneed = base;
-    }
-    for (int e = tid; e < M; e += nthr)
-      if (s_hflag[e]) s_cls[e] = SERE_CLASS_PRIMARY;
-    __syncthreads();
-    SERE_PHASE(3);
-    // ---- per-secondary argmax over the primary set (rerouting.py:78-97,157-164): one 16-lane
-    // group per secondary u; every lane first issues all its loads of row u (independent, so
-    // they overlap), then compares ascending with strict '>' and the group reduces to the
-    // first maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
-    const int n_need = s_nneed;
+    // ---- per-secondary argmax over the primary set (rerouting.py:78-97,152-164). The needed
+    // secondaries are the experts of slots >= S that are not primary (rerouting.py:152-156):
+    // one 16-lane group per expert u (groups stride over the experts; a group skips u unless
+    // it is needed). Every lane issues all its loads of row u first (independent, so they
+    // overlap), then compares ascending with strict '>' and the group reduces to the first
+    // maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
+    // The group leader also writes u's class (primary / critical / redirected).
     const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
-    for (int base = 0; base < n_need; base += ngrp) {
-      const int li = base + grp;
-      const bool have = li < n_need;
-      const int e = have ? s_list[li] : 0;
-      const double* row = p.sim + static_cast<size_t>(e) * M;
+    for (int base = 0; base < M; base += ngrp) {
+      const int e = base + grp;
+      const bool in = e < M;
+      const bool prim = in && s_hflag[e];
+      const bool need = in && !prim && s_sec[e];
+      if (glane == 0 && prim) s_cls[e] = SERE_CLASS_PRIMARY;
+      if (!__any_sync(0xffffffffu, need)) continue;  // warp-uniform: both half-warps skip
+      const double* row = simr + static_cast<size_t>(need ? e : 0) * M;
       double bs = -CUDART_INF;
       int bi = -1;
-      if (have) {
+      if (need) {
         for (int v0 = 0; v0 < M; v0 += 16 * 8) {
           double vals[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int v = v0 + glane + 16 * j;
-            vals[j] = v < M ? __ldg(row + v) : 0.0;
+            vals[j] = v < M ? row[v] : 0.0;
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -196,12 +204,12 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
         }
       }
 #pragma unroll
-      for (int off = 8; off > 0; off >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, bs, off, 16);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off, 16);
+      for (int off = 8; off > 0; off >>= 1) {  // within each 16-lane half (xor < 16)
+        const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
         if (oi >= 0 && (bi < 0 || os > bs || (os == bs && oi < bi))) { bs = os; bi = oi; }
       }
-      if (have && glane == 0) {
+      if (need && glane == 0) {
         if (p.rho > 0.0 && bs < p.rho) {
           s_cls[e] = SERE_CLASS_CRITICAL;  // preserved (rerouting.py:160-161)
         } else {
@@ -397,10 +405,10 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   if (warp < nwarps - 1) {
     // block prefixes out for the permute kernel (coalesced 32-bit words); padding rows of every
     // group carry no token (their FFN columns are never read): row_token = -1
-    const int tid2 = tid, nthr2 = nthr - 32;
-    for (int i = tid2; i < round_up(TB * Et, 2) / 2; i += nthr2)
+    const int nthr2 = nthr - 32;
+    for (int i = tid; i < round_up(TB * Et, 2) / 2; i += nthr2)
       reinterpret_cast<uint32_t*>(p.blk_prefix)[i] = reinterpret_cast<const uint32_t*>(s_cntb)[i];
-    for (int i = tid2; i < Et * kRowAlign; i += nthr2) {
+    for (int i = tid; i < Et * kRowAlign; i += nthr2) {
       const int e = i / kRowAlign, r = s_row0[e] + s_cnt[e] + (i - e * kRowAlign);
       if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
     }
@@ -452,10 +460,14 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 }
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream) {
-  const size_t smem = align_smem_total(p.T, p.K, p.M, p.m_local + p.n_shared);
+  AlignParams q = p;
+  const int Et = p.m_local + p.n_shared;
+  q.stage_sim = (p.mode & MODE_REROUTE) && p.sim != nullptr && (reinterpret_cast<uintptr_t>(p.sim) & 15) == 0 &&
+                (static_cast<size_t>(p.M) * p.M * 8) % 16 == 0 && align_smem_total(p.T, p.K, p.M, Et, true) <= kAlignSmemCap;
+  const size_t smem = align_smem_total(p.T, p.K, p.M, Et, q.stage_sim != 0);
   static SmemAttrCache attr;  // dynamic + ~4 KB static may cross the 48 KB default
   if (cudaError_t e = ensure_smem_attr(reroute_align_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
-  return launch_pdl((g_pdl & PDL_ALIGN) != 0, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, p);
+  return launch_pdl((g_pdl & PDL_ALIGN) != 0, reroute_align_kernel, dim3(1), dim3(kAlignThreads), smem, stream, q);
 }
 
 size_t reroute_align_smem(int T, int K, int M, int Et) { return align_smem_bytes(T, K, M, Et); }

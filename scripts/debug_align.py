@@ -41,9 +41,7 @@ def main() -> None:
     torch.cuda.synchronize()
     _lib.load().sere_debug_set_align_clocks(None)
     c = dbg.cpu().numpy()
-    n = int((c > 0).sum())
-    d = np.diff(c[:n])
-    print("reroute-only phases (cycles):", d.tolist(), "total", int(c[n - 1] - c[0]))
+    print("reroute-only (cycles): argmax", int(c[4] - c[1]), "final table", int(c[5] - c[4]), "total", int(c[5] - c[0]))
 
     from paper_2602_07616_b200.moe import ExpertBank, moe_forward_device
 
@@ -52,15 +50,19 @@ def main() -> None:
     w = torch.full((T, K), 1.0 / K, device="cuda")
     for _ in range(3):
         moe_forward_device(bank, sim, 1, 0.5, x, ids, w).check()
-    dbg.zero_()
-    _lib.load().sere_debug_set_align_clocks(dbg.data_ptr())
-    moe_forward_device(bank, sim, 1, 0.5, x, ids, w).check()
-    torch.cuda.synchronize()
-    _lib.load().sere_debug_set_align_clocks(None)
-    c = dbg.cpu().numpy()
-    names = {0: "init", 1: "load ids", 2: "need", 3: "list", 4: "argmax", 5: "final table+counts",
+    acc = np.zeros(16)
+    for _ in range(20):
+        dbg.zero_()
+        _lib.load().sere_debug_set_align_clocks(dbg.data_ptr())
+        moe_forward_device(bank, sim, 1, 0.5, x, ids, w).check()
+        torch.cuda.synchronize()
+        _lib.load().sere_debug_set_align_clocks(None)
+        cc = dbg.cpu().numpy().astype(np.float64)
+        acc += cc - cc[0]
+    c = acc / 20
+    names = {0: "init", 1: "load ids", 4: "argmax", 5: "final table+counts",
              7: "block prefix", 10: "group layout", 11: "schedule sort", 8: "unit prefix"}
-    order = [0, 1, 2, 3, 4, 5, 7, 10, 11, 8]
+    order = [0, 1, 4, 5, 7, 10, 11, 8]
     prev = c[0]
     parts = []
     for i in order[1:]:
