@@ -26,7 +26,10 @@
 
 namespace sere {
 
-constexpr int kAlignThreads = 1024;
+#ifndef SERE_ALIGN_THREADS
+#define SERE_ALIGN_THREADS 1024  // 256: the block size a fused router-tail variant would have (f1 A/B)
+#endif
+constexpr int kAlignThreads = SERE_ALIGN_THREADS;
 constexpr int kTokBlk = kTokBlkPerm;  // token block of the group row order (the permute ranks inside it)
 constexpr int kMaxGroupsSched = 320;  // >= max bank experts + shared experts (capi.cu kMaxExperts + kMaxShared)
 #define SERE_PHASE(i) do { if (p.dbg && threadIdx.x == 0) p.dbg[(i)] = clock64(); } while (0)
