@@ -63,6 +63,7 @@ def parse_args():
     ap.add_argument("--ep", choices=["p2p", "nccl"], default="p2p",
                     help="expert-parallel transport for N>1: peer-memory kernels (ep_p2p) or NCCL collectives (ep)")
     ap.add_argument("--pdl", type=int, default=None, help="sere_set_pdl bit mask (default: the library's)")
+    ap.add_argument("--l2", type=int, default=None, help="sere_set_l2 scratch L2 policy bits (default: the library's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     a = ap.parse_args()
@@ -387,6 +388,8 @@ def run_ours(args, wl):
 
     if args.pdl is not None:
         _lib.call("sere_set_pdl", int(args.pdl))
+    if args.l2 is not None:
+        _lib.call("sere_set_l2", int(args.l2))
 
     T, L = wl["T"], wl["L"]
     if world > 1:

@@ -202,6 +202,12 @@ int sere_residual_rmsnorm(float* x, const float* y, uint16_t* h_out, int T, int 
  * 2 permute, 4 FFN, 8 combine, 16 RMSNorm (31 = all; 0 = plain stream order). */
 int sere_set_pdl(int enable);
 
+/* L2 policy of the per-layer scratch (bit mask): 1 (default) the next layer's permute drops the
+ * previous layer's expert outputs from L2 (discard.global.L2) before its programmatic-launch wait,
+ * so their dead dirty lines are not written back to DRAM during the next weight stream
+ * (single-GPU calls only). Results are identical for every value. */
+int sere_set_l2(int flags);
+
 
 /* Profiling hook: when n == 6, every following layer call on this host thread records
  * events[0..4] before its five stages (align, permute, gate/up GEMM, down GEMM,

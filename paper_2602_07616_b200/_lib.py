@@ -116,6 +116,7 @@ SIGNATURES = {
     "sere_debug_set_ffn_mode": (_c_int, [_c_int]),
     "sere_debug_set_route_clocks": (_c_int, [_p]),
     "sere_set_pdl": (_c_int, [_c_int]),
+    "sere_set_l2": (_c_int, [_c_int]),
     "sere_debug_replay_ffn": (_c_int, [_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p, _c_size,
                                        _c_int, _p]),
     "sere_layer_workspace_layout": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int,

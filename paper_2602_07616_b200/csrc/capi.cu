@@ -191,7 +191,9 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
 
   stage_mark(1, stream);
   e = launch_permute(reinterpret_cast<const __nv_bfloat16*>(x), d, plan, L.Et, m_local, e_lo, ap.ids_final,
-                     ap.blk_prefix, T, K, n_shared, slot_row, row_token, L.r_max, x_pack, stream);
+                     ap.blk_prefix, T, K, n_shared, slot_row, row_token, L.r_max, x_pack, stream,
+                     sync == nullptr ? y_perm : nullptr,  // expert parallel: peers may still read it
+                     static_cast<long long>(d.ksplit_dn) * L.r_max * d.d_h_pad / 32);
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   FfnParams fp = ffn_params(bank, L, ws, activation);
@@ -218,6 +220,10 @@ namespace sere {
 #define SERE_PDL_DEFAULT 31  // all: +2.8% on the C4 step (FFN alone +2%), same-box A/B r02
 #endif
 int g_pdl = SERE_PDL_DEFAULT;  // PDL_* bits (sere_set_pdl)
+#ifndef SERE_L2_DEFAULT
+#define SERE_L2_DEFAULT 1  // L2_DISCARD_Y: +2.2% C4 SERE, +3% top-k (profiles/r02_l2_scratch_discard.txt)
+#endif
+int g_l2 = SERE_L2_DEFAULT;  // L2_* bits (sere_set_l2)
 }  // namespace sere
 
 using namespace sere;
@@ -583,6 +589,11 @@ int sere_debug_replay_ffn(const void* bank, int M, int n_shared, int d_h, int d_
 
 int sere_set_pdl(int enable) {
   g_pdl = enable & PDL_ALL;
+  return SERE_OK;
+}
+
+int sere_set_l2(int flags) {
+  g_l2 = flags & L2_ALL;
   return SERE_OK;
 }
 

@@ -84,9 +84,6 @@ constexpr int kPdlPrefetch = 4;
 #ifndef SERE_DEP_DEFER
 #define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
 #endif
-#ifndef SERE_Y_EVICT_LAST
-#define SERE_Y_EVICT_LAST 0
-#endif
 #ifndef SERE_STATIC_FIRST
 #define SERE_STATIC_FIRST 1
 #endif  // k-steps whose weights are issued before waiting on the permute kernel
@@ -540,9 +537,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         float* ycol = p.y_perm + static_cast<size_t>(U.ks) * p.r_max * ld + static_cast<size_t>(U.row0) * ld +
                       U.mt0 * 128 + q * 32 + lane;
         const bool store = !(p.dbg_mode & 4);
-#if SERE_Y_EVICT_LAST
-        const uint64_t pol_y = policy_evict_last();  // keep the expert outputs in L2 for the combine
-#endif
         for (int c0 = 16 * eg; c0 < U.n_mma; c0 += 16 * kEpiGroups) {
           uint32_t r[kMwDnMax][16];
 #pragma unroll
@@ -557,15 +551,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
                 float* yp = ycol + static_cast<size_t>(c0) * ld + j * 128;
                 if (nv >= 16) {
 #pragma unroll
-                  for (int i = 0; i < 16; ++i) {
-#if SERE_Y_EVICT_LAST
-                    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(yp), "r"(r[j][i]), "l"(pol_y)
-                                 : "memory");
-#else
-                    *yp = __uint_as_float(r[j][i]);
-#endif
-                    yp += ld;
-                  }
+                  for (int i = 0; i < 16; ++i) { *yp = __uint_as_float(r[j][i]); yp += ld; }
                 } else {
 #pragma unroll
                   for (int i = 0; i < 16; ++i) { if (i < nv) *yp = __uint_as_float(r[j][i]); yp += ld; }

@@ -130,12 +130,29 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
     const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
     int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
     int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
-    uint8_t* __restrict__ x_pack) {
+    uint8_t* __restrict__ x_pack, const float* __restrict__ y_dead, long long y_lines) {
   extern __shared__ __align__(16) uint8_t perm_smem[];
   int (*s_row)[kTokBlkPerm] = reinterpret_cast<int (*)[kTokBlkPerm]>(perm_smem);  // [K + n_shared][32]
   uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem) + (K + n_shared) * kTokBlkPerm;  // [K][m_loc] lanes
   uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] cells at earlier slots
   for (int i = threadIdx.x; i < K * m_loc; i += blockDim.x) s_bm[i] = 0u;
+  if (y_dead != nullptr) {
+    // before the PDL wait (the CTAs are resident while re-route/align runs): the previous
+    // layer's expert outputs were consumed by its combine, so their dirty lines leave L2
+    // without a DRAM write-back that would compete with this layer's weight stream
+    // Rows past the previous layer's total were never written: the plan's total (rewritten by
+    // re-route/align concurrently, so only a hint: old or new, both bound the live rows
+    // closely) limits the sweep to [0, rows) of every K-split plane of y_perm.
+    const int rows = min(r_max, max(0, *reinterpret_cast<const volatile int32_t*>(plan + P_TOTAL_ROWS)));
+    const long long lpr = d_h_pad / 32, per_split = static_cast<long long>(rows) * lpr;
+    const long long n = per_split * (y_lines / (static_cast<long long>(r_max) * lpr));
+    const long long nthr = static_cast<long long>(gridDim.x) * gridDim.y * blockDim.x;
+    for (long long i = (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+         i < n; i += nthr) {
+      const long long s = i / per_split, j = i - s * per_split;
+      l2_discard128(y_dead + (s * r_max * lpr + j) * 32);
+    }
+  }
   pdl_wait();
   pdl_trigger();
   if (plan[P_STATUS] != 0) return;
@@ -219,7 +236,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
 
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
                            const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
-                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream) {
+                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream,
+                           const float* y_dead, long long y_lines) {
   if (T <= 0) return cudaSuccess;
   if (K + n_shared > kPermMaxSlots) return cudaErrorInvalidValue;
   const size_t smem = permute_smem_bytes(K, n_shared, m_loc);
@@ -227,7 +245,8 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
   if (cudaError_t e = ensure_smem_attr(permute_kernel, smem, attr, 32 * 1024); e != cudaSuccess) return e;
   const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
   return launch_pdl((g_pdl & PDL_PERMUTE) != 0, permute_kernel, grid, dim3(kPermThreads), smem, stream, x, d.d_h, d.d_h_pad, plan, Et,
-                    m_loc, e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack);
+                    m_loc, e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack,
+                    (g_l2 & L2_DISCARD_Y) ? y_dead : nullptr, y_lines);
 }
 
 // ------------------------------------------------------------------ combine
@@ -267,6 +286,8 @@ __device__ __forceinline__ int ep_owner(const EpPeers& ep, int e) {
   while (o + 1 < ep.world && e >= ep.e_lo[o + 1]) ++o;
   return o;
 }
+
+
 
 __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __restrict__ y_perm, int ksplit, int r_max,
                                                       int d_h, int d_h_pad, const int32_t* __restrict__ plan,

@@ -221,6 +221,14 @@ __device__ __forceinline__ bool ep_wait(const EpSync& s) {
 // programmatic dependent launch per layer-chain kernel (sere_set_pdl bit mask)
 enum : int { PDL_ALIGN = 1, PDL_PERMUTE = 2, PDL_FFN = 4, PDL_COMBINE = 8, PDL_RMSNORM = 16, PDL_ALL = 31 };
 extern int g_pdl;  // capi.cu
+// L2 policy for the per-layer scratch (sere_set_l2 bit mask). y_perm (the fp32 expert outputs)
+// is rewritten every layer at the same addresses, so its dirty lines are dead once the combine
+// has read them; written back to DRAM they cost ~30 MB of HBM writes per C4 layer, competing with
+// the next layer's weight stream (profiles/r02_l2_scratch_discard.txt).
+//   L2_DISCARD_Y: the next layer's permute CTAs drop the previous expert outputs from L2
+//                 (discard.global.L2) before their PDL wait, while re-route/align runs
+enum : int { L2_DISCARD_Y = 1, L2_ALL = 1 };
+extern int g_l2;  // capi.cu
 
 cudaError_t launch_reroute_align(const AlignParams& p, cudaStream_t stream);
 size_t reroute_align_smem(int T, int K, int M, int Et);
@@ -228,7 +236,8 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
                         const Dims& d, int Et, int first, uint8_t* bank, int unpack, cudaStream_t stream);
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
                            const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
-                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream);
+                           int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream,
+                           const float* y_dead = nullptr, long long y_lines = 0);
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,

@@ -105,6 +105,13 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// dropping dead lines from L2 (no write-back)
+// the 128-B line at p (128-B aligned) leaves L2 without being written back; later reads
+// of it are undefined until it is written again
+__device__ __forceinline__ void l2_discard128(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // -------------------------------- bulk async copy global -> shared (TMA unit)
 // bytes must be a multiple of 16, both addresses 16-B aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
