@@ -126,17 +126,20 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
 
   // ---- load + validate ids (rerouting.py:111-114 / moe.py:299-300); lane = token, no div/mod
   const bool vec = (K & 3) == 0 && (reinterpret_cast<uintptr_t>(p.ids_in) & 15) == 0;
-  // s_ids is column-major [K][T] so that lane = token accesses are bank-conflict free
-  for (int t = tid; t < T; t += nthr) {
-    const int32_t* src = p.ids_in + static_cast<size_t>(t) * K;
+  // s_ids is column-major [K][T] so that lane = token accesses are bank-conflict free. One
+  // item per (token, 4-slot quad): T * ceil(K/4) items keep every thread busy
+  {
+    const int nq = (K + 3) >> 2;
     bool bad = false;
-    for (int k0 = 0; k0 < K; k0 += 4) {
+    for (int it = tid; it < T * nq; it += nthr) {
+      const int t = it / nq, k0 = (it - t * nq) * 4;
+      const int32_t* src = p.ids_in + static_cast<size_t>(t) * K + k0;
       int v4[4];
       if (vec) {
-        const int4 q = __ldg(reinterpret_cast<const int4*>(src + k0));
+        const int4 q = __ldg(reinterpret_cast<const int4*>(src));
         v4[0] = q.x; v4[1] = q.y; v4[2] = q.z; v4[3] = q.w;
       } else {
-        for (int j = 0; j < 4; ++j) v4[j] = k0 + j < K ? __ldg(src + k0 + j) : 0;
+        for (int j = 0; j < 4; ++j) v4[j] = k0 + j < K ? __ldg(src + j) : 0;
       }
       for (int j = 0; j < 4 && k0 + j < K; ++j) {
         const int k = k0 + j, v = v4[j];
@@ -175,39 +178,40 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
   if (reroute) {
     // ---- per-secondary argmax over the primary set (rerouting.py:78-97,152-164). The needed
     // secondaries are the experts of slots >= S that are not primary (rerouting.py:152-156):
-    // one 16-lane group per expert u (groups stride over the experts; a group skips u unless
+    // one 8-lane group per expert u (128 groups: M <= 128 in one round; a group skips u unless
     // it is needed). Every lane issues all its loads of row u first (independent, so they
     // overlap), then compares ascending with strict '>' and the group reduces to the first
     // maximum (larger value, then lower index) -- the ascending strict-'>' scan's answer.
     // The group leader also writes u's class (primary / critical / redirected).
-    const int grp = tid >> 4, glane = tid & 15, ngrp = nthr >> 4;
+    constexpr int kGl = 8, kVals = 16;
+    const int grp = tid / kGl, glane = tid % kGl, ngrp = nthr / kGl;
     for (int base = 0; base < M; base += ngrp) {
       const int e = base + grp;
       const bool in = e < M;
       const bool prim = in && s_hflag[e];
       const bool need = in && !prim && s_sec[e];
       if (glane == 0 && prim) s_cls[e] = SERE_CLASS_PRIMARY;
-      if (!__any_sync(0xffffffffu, need)) continue;  // warp-uniform: both half-warps skip
+      if (!__any_sync(0xffffffffu, need)) continue;  // warp-uniform: the warp's 4 groups skip together
       const double* row = simr + static_cast<size_t>(need ? e : 0) * M;
       double bs = -CUDART_INF;
       int bi = -1;
       if (need) {
-        for (int v0 = 0; v0 < M; v0 += 16 * 8) {
-          double vals[8];
+        for (int v0 = 0; v0 < M; v0 += kGl * kVals) {
+          double vals[kVals];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int v = v0 + glane + 16 * j;
+          for (int j = 0; j < kVals; ++j) {
+            const int v = v0 + glane + kGl * j;
             vals[j] = v < M ? row[v] : 0.0;
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int v = v0 + glane + 16 * j;
+          for (int j = 0; j < kVals; ++j) {
+            const int v = v0 + glane + kGl * j;
             if (v < M && s_hflag[v] && vals[j] > bs) { bs = vals[j]; bi = v; }
           }
         }
       }
 #pragma unroll
-      for (int off = 8; off > 0; off >>= 1) {  // within each 16-lane half (xor < 16)
+      for (int off = kGl / 2; off > 0; off >>= 1) {  // within each 8-lane group (xor < 8)
         const double os = __shfl_xor_sync(0xffffffffu, bs, off);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
         if (oi >= 0 && (bi < 0 || os > bs || (os == bs && oi < bi))) { bs = os; bi = oi; }
@@ -415,33 +419,32 @@ __global__ void __launch_bounds__(kAlignThreads, 1) reroute_align_kernel(AlignPa
       const int e = i / kRowAlign, r = s_row0[e] + s_cnt[e] + (i - e * kRowAlign);
       if (s_row0[e] >= 0 && r < s_row0[e] + round_up(s_cnt[e], kRowAlign)) p.row_token[r] = -1;
     }
-  } else {  // unit prefixes over the schedule order
+  } else {  // unit prefixes over the schedule order (one warp)
     // A small active set leaves SMs idle for the whole gate/up phase (Qwen3 T=128 after SERE:
     // 31 groups x 3 two-block units = 93 units for 148 SMs, every group's h complete only at
     // the end of it). Then the first groups in schedule order (the largest) take one-block
     // gate/up units while the total still fits one wave: they finish in half the time, and
-    // their down units (first in the down order) fill the SMs that free up.
-    if (lane == 0) {
-      int tot = 0;
-      for (int i = 0; i < G; ++i) tot += s_ugu[i];
-      for (int i = 0; i < G && tot < p.ffn_ctas; ++i) {
-        const int u1 = group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, 1);
-        if (tot + u1 - s_ugu[i] > p.ffn_ctas) break;
-        tot += u1 - s_ugu[i];
-        s_ugu[i] = -u1;  // negative: one-block units
-      }
-    }
-    __syncwarp();
-    int gu_base = 0, dn_base = 0;
+    // their down units (first in the down order) fill the SMs that free up. Greedy in schedule
+    // order: group i converts iff tot + D(i-1) < ffn_ctas and tot + D(i) <= ffn_ctas, D = the
+    // inclusive prefix of the conversions' extra units (>= 0, so the first refusal ends it).
+    int tot = 0;
+    for (int c0 = 0; c0 < G; c0 += 32) tot += c0 + lane < G ? s_ugu[c0 + lane] : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+    int gu_base = 0, dn_base = 0, d_base = 0;
     for (int c0 = 0; c0 < G; c0 += 32) {
       const int i = c0 + lane;
-      int ugu = 0, udn = 0;
+      int ugu = 0, udn = 0, dlt = 0;
       if (i < G) {
         ugu = s_ugu[i];
         udn = s_udn[i];
-        plan[po.mw_gu + i] = ugu < 0 ? 1 : kMwGuMax;
-        ugu = ugu < 0 ? -ugu : ugu;
+        dlt = group_units_gu(s_gpad[s_sched[i]], p.tiles_gu, 1) - ugu;
       }
+      const int d_in = d_base + warp_incl_scan(dlt);
+      const bool one = i < G && tot + d_in - dlt < p.ffn_ctas && tot + d_in <= p.ffn_ctas;
+      d_base = __shfl_sync(0xffffffffu, d_in, 31);
+      if (one) ugu += dlt;
+      if (i < G) plan[po.mw_gu + i] = one ? 1 : kMwGuMax;
       const int gu_in = warp_incl_scan(ugu), dn_in = warp_incl_scan(udn);
       if (i < G) {
         plan[po.unit_off_gu + i] = gu_base + gu_in - ugu;
