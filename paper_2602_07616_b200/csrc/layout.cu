@@ -130,12 +130,42 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
     const __nv_bfloat16* __restrict__ x, int d_h, int d_h_pad, const int32_t* __restrict__ plan, int Et, int m_loc,
     int e_lo, const int32_t* __restrict__ ids_final, const uint16_t* __restrict__ blk_prefix, int T, int K,
     int n_shared, int32_t* __restrict__ slot_row, int32_t* __restrict__ row_token, int r_max,
-    uint8_t* __restrict__ x_pack, const float* __restrict__ y_dead, long long y_lines) {
+    uint8_t* __restrict__ x_pack, const float* __restrict__ y_dead, long long y_lines, int x_early) {
   extern __shared__ __align__(16) uint8_t perm_smem[];
   int (*s_row)[kTokBlkPerm] = reinterpret_cast<int (*)[kTokBlkPerm]>(perm_smem);  // [K + n_shared][32]
   uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem) + (K + n_shared) * kTokBlkPerm;  // [K][m_loc] lanes
   uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] cells at earlier slots
   for (int i = threadIdx.x; i < K * m_loc; i += blockDim.x) s_bm[i] = 0u;
+  const int tb = blockIdx.x, j = blockIdx.y;
+  const int t0 = tb * kTokBlkPerm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // this CTA's slice of its tokens' rows: x does not depend on the predecessor (it was final
+  // before the re-route/align kernel started), so single-GPU the loads are in flight before
+  // the PDL wait; expert parallel, peers' rows are ordered by the barrier inside align
+  const int cpr = d_h_pad / 8;  // 16-B pieces per row
+  const int q = j * 32 + lane;
+  uint4 v[kPermTokPerWarp];
+  auto load_rows = [&]() {
+    const bool vec = (d_h & 7) == 0;
+#pragma unroll
+    for (int i = 0; i < kPermTokPerWarp; ++i) {
+      const int l = warp * kPermTokPerWarp + i, t = t0 + l;
+      const int k0 = q * 8;
+      v[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (q < cpr && t < T && k0 < d_h) {
+        const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
+        if (vec) {
+          v[i] = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+          alignas(16) __nv_bfloat16 tmp[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) tmp[e] = (k0 + e < d_h) ? src[e] : __float2bfloat16(0.f);
+          v[i] = *reinterpret_cast<uint4*>(tmp);
+        }
+      }
+    }
+  };
+  if (x_early) load_rows();
   if (y_dead != nullptr) {
     // before the PDL wait (the CTAs are resident while re-route/align runs): the previous
     // layer's expert outputs were consumed by its combine, so their dirty lines leave L2
@@ -156,9 +186,7 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
   pdl_wait();
   pdl_trigger();
   if (plan[P_STATUS] != 0) return;
-  const int tb = blockIdx.x, j = blockIdx.y;
-  const int t0 = tb * kTokBlkPerm;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!x_early) load_rows();
   const int nslot = K + n_shared;
   const int32_t* erow0 = plan + plan_offsets(Et).erow0;
   const int t_lane = t0 + lane;
@@ -199,29 +227,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
     }
   }
   // gather: lane owns 16-B piece q of the slice; tokens loaded first (all in flight), then stored
-  const int cpr = d_h_pad / 8;  // 16-B pieces per row
-  const int q = j * 32 + lane;
   if (q >= cpr) return;
   const int kt = q >> 3, c = q & 7;
-  const bool vec = (d_h & 7) == 0;
-  uint4 v[kPermTokPerWarp];
-#pragma unroll
-  for (int i = 0; i < kPermTokPerWarp; ++i) {
-    const int l = warp * kPermTokPerWarp + i, t = t0 + l;
-    const int k0 = q * 8;
-    v[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (t < T && k0 < d_h) {
-      const __nv_bfloat16* src = x + static_cast<size_t>(t) * d_h + k0;
-      if (vec) {
-        v[i] = __ldg(reinterpret_cast<const uint4*>(src));
-      } else {
-        alignas(16) __nv_bfloat16 tmp[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) tmp[e] = (k0 + e < d_h) ? src[e] : __float2bfloat16(0.f);
-        v[i] = *reinterpret_cast<uint4*>(tmp);
-      }
-    }
-  }
   uint8_t* dst_kt = x_pack + static_cast<size_t>(kt) * r_max * 128;
 #pragma unroll
   for (int i = 0; i < kPermTokPerWarp; ++i) {
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
                            const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
                            int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream,
-                           const float* y_dead, long long y_lines) {
+                           const float* y_dead, long long y_lines, bool x_early) {
   if (T <= 0) return cudaSuccess;
   if (K + n_shared > kPermMaxSlots) return cudaErrorInvalidValue;
   const size_t smem = permute_smem_bytes(K, n_shared, m_loc);
@@ -246,7 +253,7 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
   const dim3 grid((T + kTokBlkPerm - 1) / kTokBlkPerm, (d.d_h_pad / 8 + 31) / 32);
   return launch_pdl((g_pdl & PDL_PERMUTE) != 0, permute_kernel, grid, dim3(kPermThreads), smem, stream, x, d.d_h, d.d_h_pad, plan, Et,
                     m_loc, e_lo, ids_final, blk_prefix, T, K, n_shared, slot_row, row_token, r_max, x_pack,
-                    (g_l2 & L2_DISCARD_Y) ? y_dead : nullptr, y_lines);
+                    (g_l2 & L2_DISCARD_Y) ? y_dead : nullptr, y_lines, x_early ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ combine

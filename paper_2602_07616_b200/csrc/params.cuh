@@ -237,7 +237,7 @@ cudaError_t launch_pack(const __nv_bfloat16* wg, const __nv_bfloat16* wu, const 
 cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t* plan, int Et, int m_loc, int e_lo,
                            const int32_t* ids_final, const uint16_t* blk_prefix, int T, int K, int n_shared,
                            int32_t* slot_row, int32_t* row_token, int r_max, uint8_t* x_pack, cudaStream_t stream,
-                           const float* y_dead = nullptr, long long y_lines = 0);
+                           const float* y_dead = nullptr, long long y_lines = 0, bool x_early = false);
 cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const int32_t* plan,
                            const int32_t* slot_row, const float* w, int T, int K, int n_shared, float* y,
                            __nv_bfloat16* y_bf16, float* x_res, __nv_bfloat16* h_next, float eps,
