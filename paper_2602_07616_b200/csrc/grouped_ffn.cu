@@ -101,7 +101,7 @@ struct __align__(16) FfnSmemTail {
   uint64_t q_full[kQueue];
   uint64_t q_empty[kQueue];
   int32_t queue[kQueue];
-  int32_t e_page[kEntries], e_np[kEntries];  // producer: pages held by in-flight k-steps
+  int32_t e_grans[kEntries];  // producer: granules held by each in-flight k-step (incl. a wrap's skipped tail)
   int32_t t_col[kMmaWarps][kTq], t_need[kMmaWarps][kTq];  // MMA: TMEM columns of in-flight units
   uint32_t tmem_base;
   int32_t n_groups, units_gu, units_dn;
@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int qs = 0, nu = 0, head = 0, kstep = 0, oldest = 0;
+      int ring_free = kGrans;  // granules not held by in-flight k-steps
+      int e = 0, e_old = 0;     // barrier entries of the next and the oldest in-flight k-step
+      uint32_t ph_old = 0;      // parity of the oldest one's empty barrier
       uint32_t qph = 0;
       unsigned long long w_empty = 0, w_dep = 0, w_q = 0, w_empty_dn = 0;
       // PDL: weights do not depend on the preceding kernel (permute), so the first k-steps'
@@ -332,23 +335,22 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int np = kstep_grans(U, nk);
           const size_t a_off = static_cast<size_t>(nk) * bgr * kGranBytes;  // A tiles follow the nk B tiles
           const uint32_t tx = nk * (b_bytes + ((p.dbg_mode & 1) ? 0u : static_cast<uint32_t>(U.mwu) * a_copy));
-          if (head + np > kGrans) head = 0;
-          // release in FIFO order until this k-step's entry and pages are free of every
-          // in-flight k-step (after a wrap the overlap can be with the youngest ones)
-          for (;;) {
-            bool busy = kstep - oldest >= kEntries;
-            for (int s2 = oldest; !busy && s2 < kstep; ++s2)
-              busy = ranges_overlap(head, np, tail->e_page[s2 % kEntries], tail->e_np[s2 % kEntries]);
-            if (!busy) break;
+          // the ring is allocated and released in FIFO order, so the in-flight k-steps hold one
+          // contiguous arc and a count of free granules decides admission (a k-step that would
+          // cross the end of the ring starts at 0 and also holds the skipped tail)
+          const bool wrap = head + np > kGrans;
+          const int hold = (wrap ? kGrans - head : 0) + np;
+          while (kstep - oldest >= kEntries || ring_free < hold) {
             // an in-flight k-step can only complete once its deferred activation copy is issued
             if (!pdl_done || dep_g >= 0) pdl_flush();
-            mbar_wait_timed(&tail->empty[oldest % kEntries], static_cast<uint32_t>(oldest / kEntries) & 1u,
-                            acc_empty ? (U.dn ? &w_empty_dn : acc_empty) : nullptr);
+            mbar_wait_timed(&tail->empty[e_old], ph_old, acc_empty ? (U.dn ? &w_empty_dn : acc_empty) : nullptr);
+            ring_free += tail->e_grans[e_old];
             ++oldest;
+            if (++e_old == kEntries) { e_old = 0; ph_old ^= 1u; }
           }
-          const int e = kstep % kEntries;
-          tail->e_page[e] = head;
-          tail->e_np[e] = np;
+          if (wrap) head = 0;
+          ring_free -= hold;
+          tail->e_grans[e] = hold;
           uint8_t* pg = smem + static_cast<size_t>(head) * kGranBytes;
           mbar_arrive_expect_tx(&tail->full[e], tx);
           if (!(p.dbg_mode & 1)) {
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
             }
           }
           head += np;
+          if (++e == kEntries) e = 0;
         }
         if (!pdl_done || dep_g >= 0) pdl_flush();
         if (ut) ut[3] = globaltimer_ns();
@@ -393,6 +396,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       // a % kMmaWarps == mi; both walk every k-step (full/empty barriers count both)
       const int mi = warp - 1;
       int qs = 0, iter = 0, head = 0, kstep = 0, tcol = 0, oldest = 0;
+      int e = 0;          // barrier entry of the k-step
+      uint32_t eph = 0;   // its full-barrier parity
       uint32_t qph = 0;
       unsigned long long w_full = 0, w_tmem = 0, nks = 0, w_full_dn = 0, w_tmem_dn = 0, nks_dn = 0;
       unsigned long long* acc_full = (tr && mi == 0) ? &w_full : nullptr;
@@ -436,8 +441,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           const int np = kstep_grans(U, nk);
           const uint32_t a_off = static_cast<uint32_t>(nk * bgr * kGranBytes);
           if (head + np > kGrans) head = 0;
-          const int e = kstep % kEntries;
-          mbar_wait_timed(&tail->full[e], static_cast<uint32_t>(kstep / kEntries) & 1u,
+          mbar_wait_timed(&tail->full[e], eph,
                           acc_full ? (U.dn ? &w_full_dn : acc_full) : nullptr);
           nks_dn += U.dn;
           tc_fence_after();
@@ -462,6 +466,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           }
           ++nks;
           umma_commit(&tail->empty[e]);
+          if (++e == kEntries) { e = 0; eph ^= 1u; }
           head += np;
         }
         umma_commit(&tail->tfull[iter % kTq]);
