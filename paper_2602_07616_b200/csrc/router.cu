@@ -200,7 +200,7 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
     float* lgt = part + my_t0 * M;  // my tokens' logits, summed in place
     for (int i = tid; i < my_rows * M; i += blockDim.x) {
       const int r = i / M;
-      const float b = bias ? __ldg(bias + i % M) : 0.f;
+      const float b = bias ? bias[i % M] : 0.f;  // shared memory (tcgen05 path) or global
       float pv[kRcMaxSplit];
 #pragma unroll
       for (int q = 0; q < kRcMaxSplit; ++q)
@@ -231,6 +231,7 @@ __device__ __forceinline__ void route_finish(uint8_t* rsm, float* part, uint64_t
       const float lv = lgt[i];
       const float4* row = reinterpret_cast<const float4*>(lgt + r * M);
       int rank = 0;
+#pragma unroll 8
       for (int u4 = 0; u4 < M / 4; ++u4) {
         const float4 q4 = row[u4];
         const int u = u4 * 4;
@@ -462,6 +463,10 @@ __global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat1
                    "l"(src), "r"(avail)
                    : "memory");
     }
+  // the bias is static too: staged before the wait, so the logit reduction reads shared memory
+  __shared__ float s_bias[256];
+  if (bias)
+    for (int i = tid; i < M; i += blockDim.x) s_bias[i] = __ldg(bias + i);
   RC_PROBE(1);
   pdl_wait();  // x = the previous layer's RMSNorm output; ids/weights are read by its kernels
   pdl_trigger();
@@ -517,7 +522,8 @@ __global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat1
     tmem_dealloc(tmem, 64);
   }
   RC_PROBE(3);
-  route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias, ids, weights, logits_out, dbg, ep, kRtTok);
+  route_finish(rsm, part, s_gather, S, split, t0, nt_valid, M, K, bias ? s_bias : nullptr, ids, weights, logits_out,
+               dbg, ep, kRtTok);
   route_ep_arrive(ep);
 }
 
