@@ -122,8 +122,10 @@ constexpr int kPermMaxSlots = 64;       // K + n_shared (K <= 32, n_shared <= 31
 constexpr int kPermTokPerWarp = kTokBlkPerm / (kPermThreads / 32);
 
 __host__ __device__ inline size_t permute_smem_bytes(int K, int n_shared, int m_loc) {
-  // rows [K + n_shared][32] int32, lane masks u32 + slot prefixes u16 [K][m_loc]
-  return static_cast<size_t>(K + n_shared) * kTokBlkPerm * 4 + static_cast<size_t>(K) * m_loc * (4 + 2);
+  // rows [K + n_shared][32] int32, lane masks u32 + slot prefixes u16 [K][m_loc], then the
+  // block's first row per expert int32 [m_loc + n_shared]
+  return static_cast<size_t>(K + n_shared) * kTokBlkPerm * 4 + static_cast<size_t>(K) * m_loc * 4 +
+         static_cast<size_t>(round_up(K * m_loc, 2)) * 2 + static_cast<size_t>(m_loc + n_shared) * 4;
 }
 
 __global__ void __launch_bounds__(kPermThreads) permute_kernel(
@@ -135,6 +137,7 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
   int (*s_row)[kTokBlkPerm] = reinterpret_cast<int (*)[kTokBlkPerm]>(perm_smem);  // [K + n_shared][32]
   uint32_t* s_bm = reinterpret_cast<uint32_t*>(perm_smem) + (K + n_shared) * kTokBlkPerm;  // [K][m_loc] lanes
   uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_bm + K * m_loc);    // [K][m_loc] cells at earlier slots
+  int* s_base = reinterpret_cast<int*>(s_pre + round_up(K * m_loc, 2));  // [m_loc + n_shared] block's first rows
   for (int i = threadIdx.x; i < K * m_loc; i += blockDim.x) s_bm[i] = 0u;
   const int tb = blockIdx.x, j = blockIdx.y;
   const int t0 = tb * kTokBlkPerm;
@@ -191,6 +194,10 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
   const int32_t* erow0 = plan + plan_offsets(Et).erow0;
   const int t_lane = t0 + lane;
   __syncthreads();
+  // the block's first row of every local expert (group start + rows of earlier token blocks),
+  // loaded in the same round trip as the ids
+  for (int i = threadIdx.x; i < m_loc + n_shared; i += blockDim.x)
+    s_base[i] = __ldg(erow0 + i) + (i < m_loc ? static_cast<int>(__ldg(blk_prefix + static_cast<size_t>(tb) * Et + i)) : 0);
   for (int k = warp; k < K; k += kPermThreads / 32) {  // warp = slot, lane = token
     const int e = t_lane < T ? __ldg(ids_final + static_cast<size_t>(t_lane) * K + k) : -1;
     const int el = (e >= e_lo && e < e_lo + m_loc) ? e - e_lo : -1;  // -1: another rank's expert (EP)
@@ -209,12 +216,10 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(
   const unsigned lt = (1u << lane) - 1u;
   for (int k = warp; k < K; k += kPermThreads / 32) {
     const int el = s_row[k][lane];
-    s_row[k][lane] = el < 0 ? -1
-                            : __ldg(erow0 + el) + __ldg(blk_prefix + static_cast<size_t>(tb) * Et + el) +
-                                  s_pre[k * m_loc + el] + __popc(s_bm[k * m_loc + el] & lt);
+    s_row[k][lane] = el < 0 ? -1 : s_base[el] + s_pre[k * m_loc + el] + __popc(s_bm[k * m_loc + el] & lt);
   }
   for (int s2 = warp; s2 < n_shared; s2 += kPermThreads / 32)  // shared experts: every token, in token order
-    s_row[K + s2][lane] = t_lane < T ? __ldg(erow0 + m_loc + s2) + t_lane : -1;
+    s_row[K + s2][lane] = t_lane < T ? s_base[m_loc + s2] + t_lane : -1;
   __syncthreads();
   if (j == 0) {
     for (int i = threadIdx.x; i < kTokBlkPerm * nslot; i += blockDim.x) {
