@@ -391,9 +391,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       if (!pdl_done) pdl_flush();
     }
   } else if (warp < kEpiWarp0) {
-    if (lane == 0) {
+    {
       // ===================== MMA issuers: issuer mi takes the unit's accumulators a with
-      // a % kMmaWarps == mi; both walk every k-step (full/empty barriers count both)
+      // a % kMmaWarps == mi; both walk every k-step (full/empty barriers count both). The whole
+      // warp walks the loop converged and one elected lane issues (umma_bf16_elect)
       const int mi = warp - 1;
       int qs = 0, iter = 0, head = 0, kstep = 0, tcol = 0, oldest = 0;
       int e = 0;          // barrier entry of the k-step
@@ -401,11 +402,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       uint32_t qph = 0;
       unsigned long long w_full = 0, w_tmem = 0, nks = 0, w_full_dn = 0, w_tmem_dn = 0, nks_dn = 0;
       unsigned long long* acc_full = (tr && mi == 0) ? &w_full : nullptr;
-      if (mi != 0) tr = nullptr;  // issuer 0 keeps the trace
+      if (mi != 0 || lane != 0) tr = nullptr;  // issuer 0 keeps the trace
+      if (lane != 0) acc_full = nullptr;
       for (;; ++iter) {
         mbar_wait(&tail->q_full[qs], qph);
         const int u = tail->queue[qs];
-        mbar_arrive(&tail->q_empty[qs]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->q_empty[qs]);
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (u < 0) {
           if (tr) {
@@ -430,8 +433,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
                           tr ? (U.dn ? &w_tmem_dn : &w_tmem) : nullptr);
           ++oldest;
         }
-        tail->t_col[mi][iter % kTq] = col;
-        tail->t_need[mi][iter % kTq] = need;
+        __syncwarp();
+        if (lane == 0) {
+          tail->t_col[mi][iter % kTq] = col;
+          tail->t_need[mi][iter % kTq] = need;
+        }
+        __syncwarp();
         tc_fence_after();
         const int bgr = ktile_bgrans(U), apj = U.dn ? 1 : 2;  // A tiles per m-tile block and k-tile
         const uint32_t idesc = umma_idesc_bf16(128, U.n_mma);
@@ -458,18 +465,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
 #pragma unroll
                   for (int k = 0; k < 4; ++k) {
                     const uint32_t acc = (kt + kk > U.kt_begin || k > 0) ? 1u : 0u;
-                    umma_bf16(dj, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc, acc);
+                    umma_bf16_elect(dj, umma_desc_sw128(a_addr + 32 * k), umma_desc_sw128(b_addr + 32 * k), idesc,
+                                    acc);
                   }
                 }
               }
             }
           }
           ++nks;
-          umma_commit(&tail->empty[e]);
+          umma_commit_elect(&tail->empty[e]);
           if (++e == kEntries) { e = 0; eph ^= 1u; }
           head += np;
         }
-        umma_commit(&tail->tfull[iter % kTq]);
+        umma_commit_elect(&tail->tfull[iter % kTq]);
         if (tr && iter < kFfnTraceUnits) tr[1280 + iter] = globaltimer_ns();  // last MMA issued
       }
     }
