@@ -84,9 +84,6 @@ constexpr int kPdlPrefetch = 4;
 #ifndef SERE_DEP_DEFER
 #define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
 #endif
-#ifndef SERE_STATIC_FIRST
-#define SERE_STATIC_FIRST 1
-#endif  // k-steps whose weights are issued before waiting on the permute kernel
 static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
 struct Unit {
@@ -232,8 +229,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   // no early pdl_trigger: a combine grid resident during the FFN measurably slows it down
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===================== producer: tickets -> unit queue; bulk async copies into the page ring
+    {
+      // ===================== producer: tickets -> unit queue; bulk async copies into the page ring.
+      // The whole warp walks the loop converged (every value warp-uniform) and one elected lane
+      // issues each barrier arrival and copy, so the copies' operands reach the TMA unit without
+      // a per-copy ELECT/R2UR.BROADCAST waterfall
+      if (lane != 0) tr = nullptr;
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int qs = 0, nu = 0, head = 0, kstep = 0, oldest = 0;
@@ -261,12 +262,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           fence_proxy_async_global();  // h was written by generic stores on other SMs
           dep_g = -1;
         }
-        for (int i = 0; i < n_pend; ++i)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-              "%4;" ::"r"(pend_dst[i]),
-              "l"(pend_src[i]), "r"(pend_bytes[i]), "r"(pend_bar[i]), "l"(pol_x)
-              : "memory");
+        for (int i = 0; i < n_pend; ++i) bulk_g2s_elect(pend_dst[i], pend_src[i], pend_bytes[i], pend_bar[i], pol_x);
         n_pend = 0;
         pdl_done = true;
       };
@@ -274,18 +270,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
       for (;; ++nu) {
         // the first unit of CTA b is ticket b (no atomic round trip before the first copy);
         // the counter hands out tickets from gridDim.x on
-#if SERE_STATIC_FIRST
-        const int u = units_total <= 0 ? 0 : nu == 0 ? static_cast<int>(blockIdx.x)
-                                                     : static_cast<int>(gridDim.x) + atomicAdd(plan + P_TICKET, 1);
-#else
-        const int u = units_total > 0 ? atomicAdd(plan + P_TICKET, 1) : 0;
-#endif
+        int tk = 0;
+        if (lane == 0 && units_total > 0 && nu > 0) tk = atomicAdd(plan + P_TICKET, 1);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        const int u = units_total <= 0 ? 0 : nu == 0 ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x) + tk;
         unsigned long long* ut = (tr && nu < kFfnTraceUnits) ? tr + 8 + 4 * nu : nullptr;
         if (ut) { ut[0] = u; ut[1] = globaltimer_ns(); }
         const bool done = u >= units_total;
         mbar_wait_timed(&tail->q_empty[qs], qph ^ 1u, tr ? &w_q : nullptr);
-        tail->queue[qs] = done ? -1 : u;
-        mbar_arrive(&tail->q_full[qs]);
+        if (lane == 0) {
+          tail->queue[qs] = done ? -1 : u;
+          mbar_arrive(&tail->q_full[qs]);
+        }
+        __syncwarp();
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (done) {
           if (tr) { tr[1] = w_empty + w_empty_dn; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; tr[1018] = w_empty_dn; }
@@ -352,19 +349,20 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           ring_free -= hold;
           tail->e_grans[e] = hold;
           uint8_t* pg = smem + static_cast<size_t>(head) * kGranBytes;
-          mbar_arrive_expect_tx(&tail->full[e], tx);
+          mbar_arrive_expect_tx_elect(&tail->full[e], tx);
+          const uint32_t bar_e = smem_u32(&tail->full[e]);
           if (!(p.dbg_mode & 1)) {
             if (U.dn) {  // k-tile kk: the unit's 1-2 adjacent m-tiles, one copy (pages kk-major)
               for (int kk = 0; kk < nk; ++kk) {
-                bulk_g2s(pg + a_off + static_cast<size_t>(kk * U.mwu) * kPageBytes,
-                         a_unit + static_cast<size_t>(kt + kk) * kW2Group * kTileBytes, U.mwu * kTileBytes,
-                         &tail->full[e], pol_w);
+                bulk_g2s_elect(smem_u32(pg + a_off + static_cast<size_t>(kk * U.mwu) * kPageBytes),
+                               a_unit + static_cast<size_t>(kt + kk) * kW2Group * kTileBytes, U.mwu * kTileBytes, bar_e,
+                               pol_w);
               }
             } else {  // feature block j at k-tiles kt..kt+nk-1: gate/up tiles, one contiguous copy
               const uint8_t* a_kt = a_unit + static_cast<size_t>(kt) * a_copy;
               for (int j = 0; j < U.mwu; ++j)
-                bulk_g2s(pg + a_off + j * nk * a_copy, a_kt + j * a_mt_stride, nk * a_copy,
-                         &tail->full[e], pol_w);
+                bulk_g2s_elect(smem_u32(pg + a_off + j * nk * a_copy), a_kt + j * a_mt_stride, nk * a_copy, bar_e,
+                               pol_w);
             }
           }
           const bool gated = !pdl_done || dep_g >= 0;
@@ -373,12 +371,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
             uint8_t* bdst = pg + static_cast<size_t>(kk * bgr) * kGranBytes;
             const uint8_t* bsrc = b_base + (static_cast<size_t>(kt + kk) * p.r_max + U.row0) * 128;
             if (pdl_done && dep_g < 0) {
-              bulk_g2s(bdst, bsrc, b_bytes, &tail->full[e], pol_x);
+              bulk_g2s_elect(smem_u32(bdst), bsrc, b_bytes, bar_e, pol_x);
             } else {
               pend_dst[n_pend] = smem_u32(bdst);
               pend_src[n_pend] = bsrc;
               pend_bytes[n_pend] = b_bytes;
-              pend_bar[n_pend] = smem_u32(&tail->full[e]);
+              pend_bar[n_pend] = bar_e;
               ++n_pend;
             }
           }
