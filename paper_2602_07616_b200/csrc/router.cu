@@ -487,17 +487,17 @@ __global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat1
   tc_fence_after();
   RC_PROBE(2);
   const uint32_t tmem = s_tmem;
-  if (tid == 0) {
+  if (warp == 0) {  // converged warp, elected issuing lane (no per-MMA ELECT/R2UR waterfall)
     const uint32_t idesc = umma_idesc_bf16(128, kRtTok);
     for (int mt = 0; mt < n_mt; ++mt)
       for (int kt = 0; kt < nkt; ++kt) {
         const uint32_t a = smem_u32(A + (mt * nkt + kt) * kRtTileA), b = smem_u32(B + kt * kRtTileB);
 #pragma unroll
         for (int k16 = 0; k16 < 4; ++k16)
-          umma_bf16(tmem + mt * kRtTok, umma_desc_sw128(a + 32 * k16), umma_desc_sw128(b + 32 * k16), idesc,
-                    (kt | k16) ? 1u : 0u);
+          umma_bf16_elect(tmem + mt * kRtTok, umma_desc_sw128(a + 32 * k16), umma_desc_sw128(b + 32 * k16), idesc,
+                          (kt | k16) ? 1u : 0u);
       }
-    umma_commit(&s_mma);
+    umma_commit_elect(&s_mma);
   }
   mbar_wait(&s_mma, 0);
   tc_fence_after();
