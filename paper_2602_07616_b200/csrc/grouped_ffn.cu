@@ -58,7 +58,11 @@ constexpr int kPageBytes = 16384;
 // n_mma/16 (a 16-row down tile 1 instead of a whole 16 KB page), so small-N k-steps keep more
 // weight bytes in flight per SM
 constexpr int kGranBytes = 2048;
-constexpr int kGrans = kPages * kPageBytes / kGranBytes;
+#ifndef SERE_RING_GRANS
+#define SERE_RING_GRANS 104
+#endif
+constexpr int kGrans = SERE_RING_GRANS;  // operand ring size in granules (104 = 13 x 16 KB)
+constexpr int kRingBytes = kGrans * kGranBytes;
 constexpr int kTileGrans = kPageBytes / kGranBytes;
 #ifndef SERE_KENTRIES
 #define SERE_KENTRIES 12
@@ -106,7 +110,7 @@ struct __align__(16) FfnSmemTail {
 
 // per-schedule-position copies of the plan (7 arrays of Et + 1)
 __host__ __device__ inline size_t ffn_smem_bytes(int Et) {
-  return 1024 /*align slack*/ + static_cast<size_t>(kPages) * kPageBytes + sizeof(FfnSmemTail) +
+  return 1024 /*align slack*/ + static_cast<size_t>(kRingBytes) + sizeof(FfnSmemTail) +
          static_cast<size_t>(7) * (Et + 1) * sizeof(int32_t);
 }
 
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
   // 1 KB alignment (SW128 atoms) by offsetting the __shared__ array itself, so the
   // compiler keeps shared-state accesses in the shared address space (LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kPages * kPageBytes);
+  FfnSmemTail* tail = reinterpret_cast<FfnSmemTail*>(smem + kRingBytes);
   int32_t* s_arr = reinterpret_cast<int32_t*>(tail + 1);
   const int E1 = p.Et + 1;
   SchedView sv{s_arr, s_arr + E1, s_arr + 2 * E1, s_arr + 3 * E1, s_arr + 4 * E1, s_arr + 5 * E1, s_arr + 6 * E1};
