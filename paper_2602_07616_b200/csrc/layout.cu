@@ -276,7 +276,10 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 #ifndef SERE_COMB_XRES_ASYNC
 #define SERE_COMB_XRES_ASYNC 1
 #endif
-constexpr int kCombBatch = 4;
+#ifndef SERE_COMB_BATCH
+#define SERE_COMB_BATCH 4
+#endif
+constexpr int kCombBatch = SERE_COMB_BATCH;  // slots whose rows are in flight at once per thread
 
 __device__ __forceinline__ float4 load_y4(const float* src, int ksplit, size_t split_stride) {
   float4 a = __ldcg(reinterpret_cast<const float4*>(src));

@@ -208,3 +208,36 @@ def test_nonfinite_token_state_raises_domain_error(cuda_device):
     xh = x.float().cpu().numpy()
     with pytest.raises(DomainError):
         moe.route_topk(router, xh)
+
+
+def test_launch_and_l2_knobs_do_not_change_results(cuda_device):
+    """sere_set_pdl (programmatic dependent launch per kernel) and sere_set_l2 (dead expert outputs
+    dropped from L2 before the next layer's permute) change timing only: the C4-shaped step's
+    residual stream is bit-identical under every setting (graph replay, 2 steps each)."""
+    import torch
+
+    from paper_2602_07616_b200 import _lib
+    from paper_2602_07616_b200.decode import DecodeModel, DecodeStep
+
+    model = DecodeModel(3, 128, 8, 2048, 768, seed=4, beta=1.0)
+    x0 = torch.randn(512, 2048, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4))
+    outs = {}
+    try:
+        for pdl, l2 in ((31, 1), (0, 0), (31, 0), (0, 1)):
+            _lib.call("sere_set_pdl", pdl)
+            _lib.call("sere_set_l2", l2)
+            st = DecodeStep(model, 512, 1, 0.5)
+            st.set_input(x0)
+            st.capture()
+            st.run()
+            st.set_input(x0)
+            st.run()
+            torch.cuda.synchronize()
+            st.check()
+            outs[(pdl, l2)] = st.x.clone()
+    finally:
+        _lib.call("sere_set_pdl", 31)
+        _lib.call("sere_set_l2", 1)
+    ref = outs[(31, 1)]
+    for k, v in outs.items():
+        assert torch.equal(v, ref), k
