@@ -53,10 +53,12 @@ def main():
     ap.add_argument("--launches", default="gpurun_out/launches.csv")
     ap.add_argument("--note", default="")
     ap.add_argument("--round", default="r02")
+    ap.add_argument("--layers", type=int, default=4, help="profile_step --layers of the capture")
+    ap.add_argument("--skip", type=int, default=1, help="ncu -s: FFN launches skipped before the capture")
     a = ap.parse_args()
     rows, units = raw(a.rep)
     lines = [f"# {a.round} ncu summary {a.tag}: ncu --set full --clock-control none --import-source on; "
-             f"profile_step --layers 2 (C4, SERE S=1 rho=0.5 beta=1). {a.note}"]
+             f"profile_step --layers {a.layers} (captured launches from index {a.skip}; C4, SERE S=1 rho=0.5 beta=1). {a.note}"]
     launches = []
     for i, r in enumerate(rows):
         if "moe_ffn" not in r.get("Kernel Name", ""):
@@ -79,9 +81,10 @@ def main():
             if ln.startswith("active experts per layer:"):
                 actives = [int(v) for v in ln.split(":", 1)[1].strip(" []").split(",")]
     for i, L in enumerate(launches):
-        if i < len(actives):
-            L["active_experts"] = actives[i]
-            L["algorithmic_bytes"] = 2 * 3 * D_H * D_M * actives[i] + 2 * 512 * D_H + 4 * 512 * D_H + 8 * 512 * 8
+        if i + a.skip < len(actives):
+            L["active_experts"] = actives[i + a.skip]
+            L["algorithmic_bytes"] = (2 * 3 * D_H * D_M * actives[i + a.skip] + 2 * 512 * D_H + 4 * 512 * D_H
+                                      + 8 * 512 * 8)
     (ROOT / f"profiles/{a.round}_ncu_summary_{a.tag}.txt").write_text("\n".join(lines) + "\n")
     if launches and all("algorithmic_bytes" in L for L in launches):
         (ROOT / f"profiles/{a.round}_ncu_traffic_{a.tag}.json").write_text(json.dumps(
