@@ -115,7 +115,10 @@ struct RouteGeom {
 
 __host__ __device__ inline RouteGeom route_geom(int d_h, int M) {
   RouteGeom g;
-  int S = (d_h + 255) / 256;
+#ifndef SERE_ROUTE_KCHUNK
+#define SERE_ROUTE_KCHUNK 256  // d_h per split CTA (8 splits at d_h = 2048)
+#endif
+  int S = (d_h + SERE_ROUTE_KCHUNK - 1) / SERE_ROUTE_KCHUNK;
   if (S > kRcMaxSplit) S = kRcMaxSplit;
   if (S < 1) S = 1;
   g.kc = round_up((d_h + S - 1) / S, 16);
