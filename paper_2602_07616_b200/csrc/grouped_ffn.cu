@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           // contiguous arc and a count of free granules decides admission (a k-step that would
           // cross the end of the ring starts at 0 and also holds the skipped tail)
           const bool wrap = head + np > kGrans;
-          const int hold = (wrap ? kGrans - head : 0) + np;
+          // (a k-step larger than the skipped tail needs the whole ring free: cap at the ring size,
+          // a conservative count that still releases exactly what it took)
+          const int hold = min(kGrans, (wrap ? kGrans - head : 0) + np);
           while (kstep - oldest >= kEntries || ring_free < hold) {
             // an in-flight k-step can only complete once its deferred activation copy is issued
             if (!pdl_done || dep_g >= 0) pdl_flush();
