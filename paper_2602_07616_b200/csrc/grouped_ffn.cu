@@ -17,11 +17,12 @@
 //  * weights live in the bank as contiguous 16 KB pre-swizzled tiles (one bulk async
 //    copy each, TMA engine); activations come from the grouped swizzled buffers
 //    (L2-resident, evict-last);
-//  * shared memory is a ring of 13 x 16 KB = 104 granules of 2 KB (an activation tile of
-//    n_mma rows takes n_mma/16 granules, a weight tile 8); a pipeline step covers kKT k-tiles (1):
-//    their B tiles and the unit's A tiles, consecutive pages, one (full, empty) mbarrier
-//    pair from an 8-entry ring and one commit, so the stream never drains across unit
-//    boundaries;
+//  * shared memory is a ring of 104 granules of 2 KB (13 x 16 KB; an activation tile of n_mma
+//    rows takes n_mma/16 granules, a weight tile 8); a pipeline step covers kKT k-tiles (1):
+//    their B tiles and the unit's A tiles, consecutive granules, one (full, empty) mbarrier
+//    pair from a 12-entry ring and one commit, so the stream never drains across unit
+//    boundaries. The ring is allocated and released in FIFO order: a free-granule count
+//    admits the next k-step in O(1);
 //  * TMEM is a ring of columns: a unit takes mw * n_mma columns, the MMA of the next
 //    unit starts as soon as no in-flight unit (4 unit slots, released in order by the
 //    epilogue) holds its columns, so epilogues overlap MMAs whenever two units fit;
@@ -30,8 +31,10 @@
 //    (padded rows descending). A down unit waits, before its first copy, until every
 //    gate/up unit of its group has published h (per-group counters in the plan,
 //    release/acquire + async-proxy fences): no grid barrier, no second launch;
-//  * warp roles: warp 0 = producer (one lane), warp 1 = MMA issuer (one lane, also owns
-//    the TMEM allocation), warps 2..9 = epilogue (TMEM lane quadrant = warp % 4, two
+//  * warp roles: warp 0 = producer, warps 1-2 = MMA issuers (warp 1 also owns the TMEM
+//    allocation; producer and issuers run converged and issue from an elected lane, so
+//    tcgen05/bulk-copy operands reach the uniform registers without per-instruction
+//    waterfall loops), warps 3..10 = epilogue (TMEM lane quadrant = warp % 4, two
 //    warps per quadrant splitting the 16-column chunks: the fp32 down-output stores
 //    otherwise hold TMEM long enough to stall the MMA issuer). Page,
 //    column and slot positions are pure functions of the unit sequence, so the three
@@ -52,7 +55,6 @@
 
 namespace sere {
 
-constexpr int kPages = 13;
 constexpr int kPageBytes = 16384;
 // The operand ring is allocated in 2 KB granules: a weight tile takes 8, an activation tile
 // n_mma/16 (a 16-row down tile 1 instead of a whole 16 KB page), so small-N k-steps keep more
