@@ -194,6 +194,44 @@ def test_baseline_shapes_vs_torch_fp32(cuda_device, cfg):
     _check_close(fused.y.double().cpu().numpy(), ref_new.double().cpu().numpy(), cfg["name"] + " sere")
 
 
+@pytest.mark.parametrize("sim_kind", ["uniform", "clustered"])
+def test_c2_threshold_retain_sweep_vs_oracle(cuda_device, sim_kind):
+    """BASELINE C2's threshold sweep (rho in {0, 0.3, 0.5, 0.7, 0.9, 1} x S in {1, 2}) on the Qwen3 layer
+    shape, both similarity constructions of the bench: re-routed ids and active set bit-exact with the
+    oracle (rerouting.py:130-171), the fused layer equal to the plain layer on the rewritten ids, and the
+    output within the absolute bar of the fp32 reference."""
+    import torch
+
+    from paper_2602_07616_b200.decode import clustered_sim, uniform_sim
+    from paper_2602_07616_b200.moe import ExpertBank, layer_forward_device, moe_forward_device
+
+    M, K, d_h, d_m, T = 128, 8, 2048, 768, 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(21)
+    bank = ExpertBank.random(M, 0, d_h, d_m, seed=13)
+    x = torch.randn(T, d_h, device="cuda", generator=g).to(torch.bfloat16)
+    logits = torch.randn(T, M, device="cuda", generator=g) + torch.randn(M, device="cuda", generator=g)
+    top = torch.topk(logits, K, dim=1)
+    ids, w = top.indices.to(torch.int32), torch.softmax(top.values, dim=1)
+    rng = np.random.default_rng(5)
+    sim = clustered_sim(rng, M) if sim_kind == "clustered" else uniform_sim(rng, M)
+    ids_np = ids.cpu().numpy()
+    for S in (1, 2):
+        for rho in (0.0, 0.3, 0.5, 0.7, 0.9, 1.0):
+            tag = f"C2 sweep {sim_kind} S={S} rho={rho}"
+            f = moe_forward_device(bank, sim, S, rho, x, ids, w)
+            f.check()
+            want = O.apply_sere(ids_np, sim, S, rho)
+            got = f.reroute.to_result()
+            np.testing.assert_array_equal(got.new_indices, want.new_indices, err_msg=tag)
+            assert got.final_active == want.final_active and got.reroute_map == want.reroute_map, tag
+            plain = layer_forward_device(bank, x, f.reroute.new_indices, w)
+            assert torch.equal(f.y, plain.y), tag
+            if rho in (0.5, 1.0):  # the fp32 reference costs a second per point: two per S
+                ref = _torch_layer_ref(bank, x, f.reroute.new_indices.long(), w)
+                _check_close(f.y.double().cpu().numpy(), ref.double().cpu().numpy(), tag)
+
+
 def test_disabled_rewrite_bit_identical_to_topk(cuda_device):
     """tests/test_acceptance.py:63-90 on the GPU: S == K and rho == 1 reproduce plain top-k bit for bit."""
     import torch
