@@ -10,10 +10,6 @@
 #include "params.cuh"
 #include "plan.cuh"
 
-// single GPU: the permute loads its token rows before its PDL wait (1) or after it (0)
-#ifndef SERE_PERM_X_EARLY
-#define SERE_PERM_X_EARLY 1
-#endif
 
 namespace sere {
 
@@ -199,7 +195,7 @@ int run_layer(const void* bank, int M, int e_lo, int m_local, int n_shared, int 
                      ap.blk_prefix, T, K, n_shared, slot_row, row_token, L.r_max, x_pack, stream,
                      sync == nullptr ? y_perm : nullptr,  // expert parallel: peers may still read it
                      static_cast<long long>(d.ksplit_dn) * L.r_max * d.d_h_pad / 32,
-                     SERE_PERM_X_EARLY && sync == nullptr);  // single GPU: x rows loaded before the PDL wait
+                     sync == nullptr);  // single GPU: x rows loaded before the PDL wait
   if (e != cudaSuccess) return SERE_ERR_CUDA;
 
   FfnParams fp = ffn_params(bank, L, ws, activation);

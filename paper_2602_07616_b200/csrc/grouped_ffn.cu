@@ -87,9 +87,6 @@ constexpr int kMmaWarps = SERE_MMA_WARPS;
 constexpr int kEpiWarp0 = 1 + kMmaWarps;
 constexpr int kFfnThreads = 32 * (1 + kMmaWarps + kEpiWarps);
 constexpr int kPdlPrefetch = 4;
-#ifndef SERE_DEP_DEFER
-#define SERE_DEP_DEFER 0  // 1 (stream a down unit's weights before its dependency) measured 1.5% slower
-#endif
 static_assert(kPageBytes == kTileBytes, "a page holds one weight tile");
 
 struct Unit {
@@ -292,12 +289,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
         if (++qs == kQueue) { qs = 0; qph ^= 1u; }
         if (done) {
           if (tr) { tr[1] = w_empty + w_empty_dn; tr[3] = nu; tr[4] = w_dep; tr[809] = w_q; tr[1018] = w_empty_dn; }
-#if SERE_PDL_COMBINE
-          // no work left for this CTA: once every CTA got here, the combine grid may launch
-          // onto the SMs the FFN has already left and stage its slots (it waits for the FFN
-          // grid to complete before touching y_perm)
-          pdl_trigger();
-#endif
           break;
         }
         const Unit U = decode_unit(u, n_groups, units_gu, sv, p);
@@ -311,7 +302,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) moe_ffn_kernel(const FfnParams
           if (ld_acquire_gpu(dep + U.g) < U.need) {
             dep_g = U.g;
             dep_need = U.need;
-            if (!SERE_DEP_DEFER) pdl_flush();  // experiment switch: wait before the weights too
+            pdl_flush();  // (streaming the weights before this wait measured 1.5% slower)
           } else {
             fence_proxy_async_global();
           }
@@ -619,10 +610,7 @@ cudaError_t launch_moe_ffn(const FfnParams& p, int num_sms, cudaStream_t stream)
   const size_t smem = ffn_smem_bytes(p.Et);
   static SmemAttrCache attr;
   if (cudaError_t e = ensure_smem_attr(moe_ffn_kernel, smem, attr, 0); e != cudaSuccess) return e;
-#ifndef SERE_PDL_FFN
-#define SERE_PDL_FFN 0
-#endif
-  return launch_pdl((g_pdl & PDL_FFN) || SERE_PDL_FFN, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
+  return launch_pdl((g_pdl & PDL_FFN) != 0, moe_ffn_kernel, dim3(num_sms), dim3(kFfnThreads), smem, stream, p);
 }
 
 size_t moe_ffn_smem(int Et) { return ffn_smem_bytes(Et); }

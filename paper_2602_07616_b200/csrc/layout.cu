@@ -273,9 +273,6 @@ cudaError_t launch_permute(const __nv_bfloat16* x, const Dims& d, const int32_t*
 // a time (16 independent 16-B loads in flight).
 // residual row fetched into shared memory by cp.async at the start of the pass (no
 // registers held while the slot gathers are in flight): combine 10.7 -> 9.4 us per C4 layer
-#ifndef SERE_COMB_XRES_ASYNC
-#define SERE_COMB_XRES_ASYNC 1
-#endif
 #ifndef SERE_COMB_BATCH
 #define SERE_COMB_BATCH 4
 #endif
@@ -312,9 +309,7 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
                                                       float* __restrict__ x_res, __nv_bfloat16* __restrict__ h_next,
                                                       float eps, const EpPeers ep, const int32_t* __restrict__ ids_rr) {
   __shared__ float s_red[16];
-#if SERE_COMB_XRES_ASYNC
   __shared__ __align__(16) float s_xr[kRowMaxThreads * kRowVec];  // this token's residual row (d_h <= 4096)
-#endif
   __shared__ const float* s_src[64];  // slot's expert-output row (nullptr: not evaluated / not owned)
   __shared__ size_t s_split[64];      // its K-split plane stride
   __shared__ float s_w[64];
@@ -365,7 +360,6 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-#if SERE_COMB_XRES_ASYNC
   // the residual row goes to shared memory with cp.async now (no registers held), so its
   // latency overlaps the slot gathers instead of following them
   const bool xr_async = x_res != nullptr && (d_h & 3) == 0 && d_h <= kRowMaxThreads * kRowVec;
@@ -376,7 +370,6 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
                    : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-#endif
   const bool vec4 = (d_h & 3) == 0;
   float ss = 0.f;
   for (int base = 0; base < d_h; base += blockDim.x * kRowVec) {
@@ -432,15 +425,9 @@ __global__ void __launch_bounds__(kRowMaxThreads) combine_kernel(const float* __
         else for (int q = 0; q < 4 && f0 + q < d_h; ++q) y_bf16[o + q] = __float2bfloat16_rn(acc[c][q]);
       }
       if (x_res) {
-#if SERE_COMB_XRES_ASYNC
         if (xr_async) asm volatile("cp.async.wait_group 0;" ::: "memory");  // own copies only: same thread
-#endif
         for (int q = 0; q < 4 && f0 + q < d_h; ++q) {
-#if SERE_COMB_XRES_ASYNC
           const float vv = (xr_async ? s_xr[f0 + q] : x_res[o + q]) + acc[c][q];
-#else
-          const float vv = x_res[o + q] + acc[c][q];
-#endif
           x_res[o + q] = vv;
           acc[c][q] = vv;
           ss = fmaf(vv, vv, ss);
@@ -491,7 +478,7 @@ cudaError_t launch_combine(const float* y_perm, const Dims& d, int r_max, const 
                            cudaStream_t stream, const EpPeers* ep, const int32_t* ids_rr) {
   if (T <= 0) return cudaSuccess;
   EpPeers none{};
-  return launch_pdl((g_pdl & PDL_COMBINE) || SERE_PDL_COMBINE, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
+  return launch_pdl((g_pdl & PDL_COMBINE) != 0, combine_kernel, dim3(T), dim3(row_threads(d.d_h)), 0, stream, y_perm, d.ksplit_dn, r_max,
                     d.d_h, d.d_h_pad, plan, slot_row, w, T, K, n_shared, y, y_bf16, x_res, h_next, eps,
                     ep ? *ep : none, ids_rr);
 }

@@ -211,13 +211,6 @@ __device__ __forceinline__ bool ep_wait(const EpSync& s) {
   return true;
 }
 
-// 1: the combine grid is launched with programmatic dependent launch and the FFN triggers
-// it when each CTA runs out of tickets, so combine CTAs start on the SMs the FFN's tail has
-// left and stage their slots. Measured within noise on the 48-layer bench (-1.2% on a
-// 24-layer kernel trace), so off by default; an early trigger slowed the FFN.
-#ifndef SERE_PDL_COMBINE
-#define SERE_PDL_COMBINE 0
-#endif
 // programmatic dependent launch per layer-chain kernel (sere_set_pdl bit mask)
 enum : int { PDL_ALIGN = 1, PDL_PERMUTE = 2, PDL_FFN = 4, PDL_COMBINE = 8, PDL_RMSNORM = 16, PDL_ALL = 31 };
 extern int g_pdl;  // capi.cu

@@ -79,11 +79,11 @@ constexpr int kTmemCols = 512;
 #define SERE_MW_GU_MAX 2
 #endif
 #ifndef SERE_MW_DN_MAX
-#define SERE_MW_DN_MAX 2  // 4 (with SERE_DN_WIDE_MAXN 64): top-k FFN -2.9%, but the SERE step +1%
+#define SERE_MW_DN_MAX 2
 #endif
 constexpr int kMwGuMax = SERE_MW_GU_MAX;  // gate/up: feature blocks of 128 (2 accumulators each; 2 measured
                                           // 5% faster than 1: 16 MMAs per k-step amortise the issue cost)
-constexpr int kMwDnMax = SERE_MW_DN_MAX;  // down: 2 x 128 features (4 for narrow groups: dn_cap)
+constexpr int kMwDnMax = SERE_MW_DN_MAX;  // down: 2 x 128 features per unit
 
 // accs = TMEM accumulators per m-tile (2 for gate/up: gate and up; 1 for down)
 __host__ __device__ inline int unit_mw(int n16, int cap, int tiles, int accs = 1) {
@@ -98,18 +98,9 @@ __host__ __device__ inline int group_units_gu(int n16, int tiles_gu, int cap = k
   const int mw = unit_mw(n16, cap, tiles_gu, 2);
   return col_blocks(n16) * ((tiles_gu + mw - 1) / mw);
 }
-#ifndef SERE_DN_SMALL_N
-#define SERE_DN_SMALL_N 0
-#endif
-#ifndef SERE_DN_WIDE_MAXN
-#define SERE_DN_WIDE_MAXN 64  // 4-wide for <= 64 rows: top-k FFN -2.9%, SERE unchanged (all widths: SERE +0.8%)
-#endif
-// down units of small groups (scheduled last) take one m-tile: they finish the step.
-// With SERE_MW_DN_MAX = 4, only groups of <= SERE_DN_WIDE_MAXN rows take 4 m-tiles (their
-// h tile is re-read half as often); wider groups keep 2
-__host__ __device__ inline int dn_cap(int n16) {
-  return n16 <= SERE_DN_SMALL_N ? 1 : (n16 <= SERE_DN_WIDE_MAXN ? kMwDnMax : (kMwDnMax > 2 ? 2 : kMwDnMax));
-}
+// down units take kMwDnMax m-tiles (4-wide units for narrow groups: top-k FFN -2.9% but the SERE
+// step +1%; one-m-tile units for the smallest groups: neutral for SERE, -7% for top-k)
+__host__ __device__ inline int dn_cap(int) { return kMwDnMax; }
 __host__ __device__ inline int group_units_dn(int n16, int tiles_dn, int ksplit_dn) {
   const int mw = unit_mw(n16, dn_cap(n16), tiles_dn);
   return col_blocks(n16) * ((tiles_dn + mw - 1) / mw) * ksplit_dn;

@@ -393,15 +393,9 @@ __global__ void __launch_bounds__(kRcThreads) route_cluster_kernel(const __nv_bf
 // SW128 tiles, B = the tile's 16 token rows, D = [128 experts x 16 tokens] fp32 in TMEM --
 // n_mt * kc/16 MMAs issued by one thread instead of 16 warps of mma.sync (which the profile
 // showed throughput-bound at ~4k cycles). Same split-K cluster and top-K tail.
-#ifndef SERE_ROUTE_TC
-#define SERE_ROUTE_TC 1
-#endif
-// 1: the tcgen05 router launches with programmatic dependent launch, so its CTAs stage the
-// static router weights while the previous kernel (combine) finishes; its outputs are
-// written after griddepcontrol.wait. -1% step time (24-layer trace, 2 reps)
-#ifndef SERE_PDL_ROUTER
-#define SERE_PDL_ROUTER 1
-#endif
+// The tcgen05 router always launches with programmatic dependent launch: its CTAs stage the
+// static router weights while the previous kernel (combine) finishes and write their outputs
+// after griddepcontrol.wait (-1% step time on a 24-layer trace)
 // tokens per cluster tile (MMA N). 32 measured slower (13.6 vs 11.1 us): half the CTAs, and
 // each CTA's top-K tail ranks twice the tokens
 constexpr int kRtTok = 16;
@@ -425,7 +419,7 @@ __host__ __device__ inline RouteTcGeom route_tc_geom(int d_h, int M) {
 }
 bool route_tc_path(int M, int K, int d_h) {
   const RouteTcGeom t = route_tc_geom(d_h, M);
-  return SERE_ROUTE_TC && route_fast_path(M, K, d_h) && M <= 256 && t.kc % 64 == 0 && t.smem <= 200 * 1024;
+  return route_fast_path(M, K, d_h) && M <= 256 && t.kc % 64 == 0 && t.smem <= 200 * 1024;
 }
 
 __global__ void __launch_bounds__(kRcThreads) route_tc_kernel(const __nv_bfloat16* __restrict__ x,
@@ -558,7 +552,7 @@ cudaError_t launch_route_mma(const __nv_bfloat16* x, const __nv_bfloat16* w_rout
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (g_pdl || SERE_PDL_ROUTER) ? 2 : 1;
+    cfg.numAttrs = 2;
     EpPeers none{};
     return cudaLaunchKernelEx(&cfg, route_tc_kernel, x, w_router, bias, T, d_h, M, K, g.kc, ids, weights,
                               logits_out, g_route_dbg, ep ? *ep : none);
